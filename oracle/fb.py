@@ -1,0 +1,372 @@
+"""fp64 oracle: Algorithm 1 (Fast FB expansion) and Algorithm 2 (steerable PCA).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  P:n = PAPER.md line n.
+
+Data conventions (shared *by definition* with the product, not by code):
+  images : (n, L, L) float, axis 0 = i1, axis 1 = i2, i = a - floor(L/2)   (Q3)
+  A      : list over k = 0..k_max of complex arrays (p_k, n); rows q, columns images
+           (the paper's A^(k))
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+from numpy.polynomial.legendre import leggauss
+from scipy.optimize import brentq
+from scipy.special import jv
+
+__all__ = [
+    "Basis", "bessel_zeros_upto", "build_basis", "gauss_legendre", "polar_grid",
+    "radial_table", "polar_ft_direct", "angular_transform", "radial_quadrature",
+    "expand", "expand_polar", "synthesize_polar", "mean_and_center",
+    "block_covariance", "covariance_partials", "finalize_covariance",
+    "block_eig", "sign_normalize", "spca_coeffs", "mp_edge", "mp_select",
+    "shrink_weights", "project", "rotate_coeffs", "reflect_coeffs",
+    "flat_index", "to_flat", "from_flat",
+]
+
+
+# --------------------------------------------------------------------------
+# O1 census: Bessel roots and the Klug-Crowther truncation
+# --------------------------------------------------------------------------
+def bessel_zeros_upto(k: int, xmax: float, step: float = 0.25) -> np.ndarray:
+    """All positive zeros R_{k,q} of J_k with R_{k,q} <= xmax, plus the first one above.
+
+    P:87 "R_{k,q} is the q-th root of the Bessel function J_k".  Bracketing by a
+    sign scan of step 0.25 (< pi, the lower bound on the spacing of consecutive
+    zeros, so each bracket holds one root; J_k has no zeros below x = k), then
+    brentq, then Newton polish with J_k' = (J_{k-1} - J_{k+1})/2.
+    """
+    x0 = max(float(k), 0.05)
+    hi = xmax + 2 * math.pi
+    roots = []
+    while not roots or roots[-1] <= xmax:
+        xs = np.arange(x0, hi + step, step)
+        v = jv(k, xs)
+        for i in np.nonzero(np.sign(v[:-1]) * np.sign(v[1:]) < 0)[0]:
+            r = brentq(lambda x: jv(k, x), xs[i], xs[i + 1], xtol=1e-14, rtol=1e-15, maxiter=200)
+            for _ in range(3):  # Newton polish
+                d = 0.5 * (jv(k - 1, r) - jv(k + 1, r))
+                r = r - jv(k, r) / d
+            roots.append(r)
+            if r > xmax:
+                break
+        x0, hi = xs[-1], hi + 4 * math.pi       # no root above xmax yet: scan further
+    return np.asarray(roots)
+
+
+@dataclass
+class Basis:
+    """Truncated FB basis for band limit c and support radius R."""
+    c: float
+    R: float
+    k_max: int
+    p: list                      # p_k, k = 0..k_max
+    zeros: list                  # zeros[k] = array of R_{k,q}, q = 1..p_k+1
+    norm: list                   # norm[k][q-1] = N_{k,q}
+    n_xi: int = 0
+    n_theta: int = 0
+
+    @property
+    def coef_off(self) -> np.ndarray:
+        return np.concatenate([[0], np.cumsum(self.p)]).astype(np.int64)
+
+    @property
+    def n_coef(self) -> int:
+        return int(sum(self.p))
+
+
+def _ceil_int(x: float) -> int:
+    # DESIGN.md reading Q4: ceil with a 1e-9 guard against representation noise.
+    return int(math.ceil(x - 1e-9))
+
+
+def build_basis(c: float, R: float) -> Basis:
+    """Census under Eq. (criterion1) R_{k,q+1} <= 2 pi c R.
+
+    p_k = #{q >= 1 : R_{k,q+1} <= 2 pi c R}; k runs 0,1,... until the first p_k = 0
+    ("k_max is the maximal possible value of k satisfying Eq. (criterion1)").
+    Also fixes n_xi = ceil(4cR), n_theta = ceil(16cR) (Alg. 1 step 1).
+    """
+    X = 2.0 * math.pi * c * R
+    p, zeros, norm = [], [], []
+    k = 0
+    while True:
+        z = bessel_zeros_upto(k, X)
+        pk = int(np.sum(z[1:] <= X)) if len(z) > 1 else 0
+        if pk == 0:
+            break
+        p.append(pk)
+        zeros.append(z[: pk + 1].copy())
+        # N_{k,q} = (c sqrt(pi) |J_{k+1}(R_{k,q})|)^{-1}
+        norm.append(1.0 / (c * math.sqrt(math.pi) * np.abs(jv(k + 1, z[:pk]))))
+        k += 1
+    return Basis(c=c, R=R, k_max=len(p) - 1, p=p, zeros=zeros, norm=norm,
+                 n_xi=_ceil_int(4 * c * R), n_theta=_ceil_int(16 * c * R))
+
+
+# --------------------------------------------------------------------------
+# O2-O4 quadrature grid and radial table
+# --------------------------------------------------------------------------
+def gauss_legendre(m: int, a: float, b: float):
+    """m-point Gauss-Legendre rule on [a, b], from numpy.leggauss."""
+    x, w = leggauss(m)
+    return a + (b - a) * (x + 1) / 2, w * (b - a) / 2
+
+
+def polar_grid(basis: Basis):
+    """xi_j (GL on [0,c], n_xi points), w_j, theta_l = 2 pi l / n_theta."""
+    xi, w = gauss_legendre(basis.n_xi, 0.0, basis.c)
+    theta = 2 * np.pi * np.arange(basis.n_theta) / basis.n_theta
+    return xi, w, theta
+
+
+def radial_table(basis: Basis, xi=None, w=None):
+    """B_k[q][j] = N_{k,q} J_k(R_{k,q} xi_j / c) xi_j w(xi_j)  (Eq. (a))."""
+    if xi is None:
+        xi, w, _ = polar_grid(basis)
+    out = []
+    for k in range(basis.k_max + 1):
+        Rk = basis.zeros[k][: basis.p[k]]
+        Nk = basis.norm[k]
+        out.append(Nk[:, None] * jv(k, np.outer(Rk, xi) / basis.c) * (xi * w)[None, :])
+    return out
+
+
+# --------------------------------------------------------------------------
+# O5 direct Fourier sum at the polar nodes (Eq. (nufft); Q1 unit prefactor)
+# --------------------------------------------------------------------------
+def polar_ft_direct(images: np.ndarray, basis: Basis, chunk: int = 4) -> np.ndarray:
+    """F(I)(xi_1, xi_2) = sum_{i1,i2} I(i1,i2) exp(-2 pi i (xi_1 i1 + xi_2 i2)).
+
+    Evaluated exactly (up to rounding) at every node (xi_j cos theta_l, xi_j sin theta_l),
+    l = 0..n_theta-1.  Nodes l < n_theta/2 are summed directly; for even n_theta the node
+    l + n_theta/2 is the negated node l, where the sum for a real image is the complex
+    conjugate (exact identity of the definition for real I).
+    Returns (n, n_xi, n_theta) complex128.
+    """
+    images = np.asarray(images, dtype=np.float64)
+    n, L, L2 = images.shape
+    assert L == L2
+    xi, _, theta = polar_grid(basis)
+    nt = basis.n_theta
+    half = nt // 2 if nt % 2 == 0 else nt
+    idx = np.arange(L) - L // 2                                   # i = a - floor(L/2)
+    k1 = np.outer(xi, np.cos(theta[:half])).ravel()               # xi_1 at nodes
+    k2 = np.outer(xi, np.sin(theta[:half])).ravel()               # xi_2 at nodes
+    E1 = np.exp(-2j * np.pi * np.outer(k1, idx))                  # (nodes, L): e^{-2pi i xi1 i1}
+    E2 = np.exp(-2j * np.pi * np.outer(k2, idx))                  # (nodes, L): e^{-2pi i xi2 i2}
+    out = np.empty((n, basis.n_xi, nt), dtype=np.complex128)
+    for s in range(0, n, chunk):
+        I = images[s:s + chunk]                                   # (b, L, L) real
+        # T[b, i1, node] = sum_{i2} I[b, i1, i2] E2[node, i2]  (real x complex via 2 real GEMMs)
+        T = (I @ E2.real.T) + 1j * (I @ E2.imag.T)
+        F = np.einsum("na,ban->bn", E1, T)                        # sum over i1
+        F = F.reshape(-1, basis.n_xi, half)
+        out[s:s + chunk, :, :half] = F
+        if half != nt:
+            out[s:s + chunk, :, half:] = np.conj(F)
+    return out
+
+
+# --------------------------------------------------------------------------
+# O6-O7 angular FFT and radial quadrature (Eqs. (1DFFT) P:189 and (a) P:195)
+# --------------------------------------------------------------------------
+def angular_transform(F: np.ndarray, k_max: int) -> np.ndarray:
+    """g^(xi_j, k) = (2 pi / n_theta) sum_l F(xi_j, theta_l) e^{-2 pi i k l / n_theta}, k=0..k_max."""
+    nt = F.shape[-1]
+    return (2 * np.pi / nt) * np.fft.fft(F, axis=-1)[..., : k_max + 1]
+
+
+def radial_quadrature(ghat: np.ndarray, basis: Basis, table=None) -> list:
+    """a_{k,q} = sum_j N_{k,q} J_k(R_{k,q} xi_j/c) g^(xi_j,k) xi_j w_j  (Eq. (a)).
+
+    ghat: (n, n_xi, k_max+1).  Returns list A[k] of (p_k, n) complex.  Im a_{0,q} := 0 (Q8).
+    """
+    if table is None:
+        table = radial_table(basis)
+    A = []
+    for k in range(basis.k_max + 1):
+        Ak = table[k] @ ghat[:, :, k].T                           # (p_k, n)
+        if k == 0:
+            Ak = Ak.real.astype(np.complex128)
+        A.append(Ak)
+    return A
+
+
+def expand_polar(F: np.ndarray, basis: Basis, table=None) -> list:
+    """Steps (1DFFT) + (a) of Alg. 1 line 4 on given polar samples F (n, n_xi, n_theta)."""
+    return radial_quadrature(angular_transform(F, basis.k_max), basis, table)
+
+
+def expand(images: np.ndarray, basis: Basis, chunk: int = 4) -> list:
+    """Algorithm 1 with the exact Fourier sum in place of the NUFFT."""
+    table = radial_table(basis)
+    parts = []
+    for s in range(0, len(images), chunk):
+        F = polar_ft_direct(images[s:s + chunk], basis, chunk)
+        parts.append(expand_polar(F, basis, table))
+    return [np.concatenate([p[k] for p in parts], axis=1) for k in range(basis.k_max + 1)]
+
+
+def synthesize_polar(A: list, basis: Basis) -> np.ndarray:
+    """P_{c,R} F(f) on the polar grid (Eq. (contapprox)), negative k by a_{-k}=conj(a_k).
+
+    F(xi_j, theta_l) = sum_k sum_q a_{k,q} N_{k,q} J_k(R_{k,q} xi_j/c) e^{i k theta_l}.
+    A[k] is (p_k, n) for k = 0..k_max; returns (n, n_xi, n_theta).
+    Used only by oracle pins (exact-recovery test).
+    """
+    xi, _, theta = polar_grid(basis)
+    n = A[0].shape[1]
+    F = np.zeros((n, basis.n_xi, basis.n_theta), dtype=np.complex128)
+    for k in range(basis.k_max + 1):
+        Rk = basis.zeros[k][: basis.p[k]]
+        rad = basis.norm[k][:, None] * jv(k, np.outer(Rk, xi) / basis.c)   # (p_k, n_xi)
+        s = A[k].T @ rad                                                    # (n, n_xi)
+        F += s[:, :, None] * np.exp(1j * k * theta)[None, None, :]
+        if k > 0:
+            s_neg = np.conj(A[k]).T @ (rad * (-1) ** k)     # psi^{-k,q} = (-1)^k J_k e^{-ik theta}
+            F += s_neg[:, :, None] * np.exp(-1j * k * theta)[None, None, :]
+    return F
+
+
+# --------------------------------------------------------------------------
+# O8 mean / covariance (Alg. 2 lines 1-4)
+# --------------------------------------------------------------------------
+def mean_and_center(A: list):
+    """a^mean_{0,q} = (1/n) sum_j a^j_{0,q}; a^i_{0,q} <- a^i_{0,q} - mean (Alg. 2 line 1)."""
+    mean = A[0].real.mean(axis=1)
+    Ac = [A[0] - mean[:, None]] + list(A[1:])
+    return mean, Ac
+
+
+def block_covariance(A: list):
+    """C^(k) = (1/n) Re{A^(k) A^(k)*} (Eq. (ck)); C^(0) = (1/n) A0 A0^* after centring."""
+    n = A[0].shape[1]
+    mean, Ac = mean_and_center(A)
+    C = [np.real(Ak @ np.conj(Ak).T) / n for Ak in Ac]
+    return mean, C
+
+
+def covariance_partials(A: list):
+    """Shard-local sums for the data-parallel form of (ck)/(ck_0):
+    S_k = sum_i Re(a_i a_i^*), s0 = sum_i a_{0,i}, n.  ("each worker is allocated a subset")."""
+    S = [np.real(Ak @ np.conj(Ak).T) for Ak in A]
+    return S, A[0].real.sum(axis=1), A[0].shape[1]
+
+
+def finalize_covariance(S: list, s0: np.ndarray, n: int):
+    """C^(0) = S_0/n - s0 s0^T/n^2 (= (1/n) sum (a0-m)(a0-m)^T); C^(k) = S_k/n."""
+    mean = s0 / n
+    C = [S[0] / n - np.outer(mean, mean)] + [Sk / n for Sk in S[1:]]
+    return mean, C
+
+
+# --------------------------------------------------------------------------
+# O9 eigendecomposition (Alg. 2 line 4)
+# --------------------------------------------------------------------------
+def sign_normalize(U: np.ndarray) -> np.ndarray:
+    """Reading Q10: make the entry of largest |u(q)| positive (ties -> lowest q)."""
+    U = U.copy()
+    for l in range(U.shape[1]):
+        q = int(np.argmax(np.abs(U[:, l])))      # argmax returns the lowest index on ties
+        if U[q, l] < 0:
+            U[:, l] = -U[:, l]
+    return U
+
+
+def block_eig(C: list):
+    """lambda^(k)_1 >= ... >= lambda^(k)_{p_k}, u^(k)_l (numpy.linalg.eigh, sorted descending)."""
+    lam, U = [], []
+    for Ck in C:
+        w, V = np.linalg.eigh(0.5 * (Ck + Ck.T))
+        o = np.argsort(-w, kind="stable")
+        lam.append(w[o])
+        U.append(sign_normalize(V[:, o]))
+    return lam, U
+
+
+# --------------------------------------------------------------------------
+# O10-O11 projection and MP filtering (Eq. (sPCAcoeff); Eq. (compselect))
+# --------------------------------------------------------------------------
+def spca_coeffs(Ac: list, U: list) -> list:
+    """c^i_{k,l} = sum_q a^i_{k,q} u_l^(k)(q): returns (p_k, n) per k."""
+    return [Uk.T @ Ak for Uk, Ak in zip(U, Ac)]
+
+
+def mp_edge(sigma2: float, p_k: int, n: int, k: int) -> float:
+    """lambda_+^(k) = sigma^2 (1 + sqrt(gamma_k))^2, gamma_0 = p_0/n, gamma_k = p_k/(2n)."""
+    gamma = p_k / n if k == 0 else p_k / (2.0 * n)
+    return sigma2 * (1.0 + math.sqrt(gamma)) ** 2
+
+
+def mp_select(lam: list, basis: Basis, n: int, sigma2: float) -> list:
+    """Eq. (compselect): keep lambda^(k)_l > sigma^2 (1 + sqrt(gamma_k))^2."""
+    return [lk > mp_edge(sigma2, basis.p[k], n, k) for k, lk in enumerate(lam)]
+
+
+def shrink_weights(lam: list, basis: Basis, n: int, sigma2: float, mode: int) -> list:
+    """Filter weights per (k,l).
+
+    mode 0: h = 1 (projection only).
+    mode 1: MP-select (Eq. compselect) then h = l/(l+sigma^2), l = (lambda - sigma^2)_+  (Q13).
+    mode 2: MP-select then spiked-model l = ((lambda - s(1+g)) + sqrt((lambda - s(1+g))^2 - 4 g s^2))/2,
+            h = l/(l+s)   (SPEC S:442 optional mode; the paper defers to [Wu13]).
+    """
+    out = []
+    for k, lk in enumerate(lam):
+        if mode == 0:
+            out.append(np.ones_like(lk))
+            continue
+        sel = lk > mp_edge(sigma2, basis.p[k], n, k)
+        if mode == 1:
+            ell = np.maximum(lk - sigma2, 0.0)
+        else:
+            g = basis.p[k] / n if k == 0 else basis.p[k] / (2.0 * n)
+            t = lk - sigma2 * (1 + g)
+            ell = 0.5 * (t + np.sqrt(np.maximum(t * t - 4 * g * sigma2 * sigma2, 0.0)))
+        h = np.where(sel, ell / (ell + sigma2) if sigma2 > 0 else 1.0, 0.0)
+        out.append(h)
+    return out
+
+
+def project(A: list, mean: np.ndarray, U: list, lam: list, basis: Basis,
+            sigma2: float, mode: int, n_total: int) -> list:
+    """Alg. 2 line 6 with optional filtering: out_k = diag(h_k) U_k^T a_k (k=0 centred)."""
+    Ac = [A[0] - mean[:, None]] + list(A[1:])
+    c = spca_coeffs(Ac, U)
+    h = shrink_weights(lam, basis, n_total, sigma2, mode)
+    return [hk[:, None] * ck for hk, ck in zip(h, c)]
+
+
+# --------------------------------------------------------------------------
+# O(2) action on coefficients (Eqs. (rot), (refl) P:292)
+# --------------------------------------------------------------------------
+def rotate_coeffs(A: list, alpha: float) -> list:
+    """a_{k,q} -> a_{k,q} e^{-i k alpha}."""
+    return [Ak * np.exp(-1j * k * alpha) for k, Ak in enumerate(A)]
+
+
+def reflect_coeffs(A: list, alpha: float = 0.0) -> list:
+    """a_{k,q} -> a_{-k,q} e^{-i k alpha} = conj(a_{k,q}) e^{-i k alpha} for real images."""
+    return [np.conj(Ak) * np.exp(-1j * k * alpha) for k, Ak in enumerate(A)]
+
+
+# --------------------------------------------------------------------------
+# layout helpers (k-major flat layout used by the C-ABI: block k at coef_off[k], rows q, cols images)
+# --------------------------------------------------------------------------
+def flat_index(basis: Basis):
+    off = basis.coef_off
+    return off
+
+
+def to_flat(A: list) -> np.ndarray:
+    """(sum_k p_k, n) complex array, block k = rows coef_off[k]..coef_off[k+1]."""
+    return np.concatenate(A, axis=0)
+
+
+def from_flat(flat: np.ndarray, basis: Basis) -> list:
+    off = basis.coef_off
+    return [flat[off[k]:off[k + 1]] for k in range(basis.k_max + 1)]
