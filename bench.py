@@ -1,0 +1,368 @@
+"""Benchmark: images/s of expansion + covariance (Alg. 1 + Alg. 2 lines 1-3 incl. the all-reduce and
+finalise) on BASELINE.json configs[2] (C3: n = 100,000 images, L = 128, R = 64, c = 1/2, fp32),
+sharded contiguously over the ranks (strong scaling: total n fixed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference]
+
+One JSON line on rank 0.  See DESIGN.md "Measurement" for every field's definition.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "images/sec (expansion+covariance, L=128) at 1/2/4/8 B200; % HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=0, help="override total images (testing only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------- clocks sampler (B200_PROFILING.md recipe)
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- per-image algorithmic work
+def work_per_image(plan, L):
+    """Algorithmic flops of K1-K3 (polar kernel) and bytes of each stage, per image."""
+    M, w, nxi, nth, kmax = plan.M, plan.w, plan.n_xi, plan.n_theta, plan.k_max
+    lg = lambda n: math.log2(n)
+    k1 = 5 * M * lg(M) * (L / 2) + 5 * M * lg(M) * (M / 4 + w)       # row FFTs (L/2 complex) + column FFTs
+    k2 = nxi * (nth // 2) * w * w * 4                                 # complex-by-real taps
+    k3 = nxi * 5 * nth * lg(nth)                                      # ring FFTs
+    ncoef = plan.n_coef
+    k4 = 4 * nxi * ncoef                                              # Eq. (a): 2 real MACs per (k,q,j)
+    k5 = 4 * float((plan.p.astype(float) ** 2).sum())                 # Re(a a^*): full (not halved) count
+    b_img, b_ghat = 4 * L * L, 8 * nxi * (kmax + 1)
+    b_coef = 8 * ncoef
+    return dict(k1=k1, k2=k2, k3=k3, k4=k4, k5=k5, polar_flops=k1 + k2 + k3,
+                polar_bytes=b_img + b_ghat, radial_bytes=b_ghat + b_coef, cov_bytes=b_coef,
+                algorithmic_bytes=b_img + b_coef)
+
+
+def cpu_baseline(cfg, seconds_target=15.0):
+    """The oracle as it stands (expansion + covariance) on a bounded sample of the same workload."""
+    import numpy as np
+    import oracle as O
+    import synth
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    sig = synth.blobs.noise_sigma(cfg)
+    imgs = synth.blob_images(cfg, 0, 2, sigma_n=sig).double().numpy()
+    t0 = time.perf_counter()
+    O.block_covariance(O.expand(imgs, basis))
+    per = (time.perf_counter() - t0) / 2
+    m = max(2, min(64, int(seconds_target / max(per, 1e-3))))
+    imgs = synth.blob_images(cfg, 0, m, sigma_n=sig).double().numpy()
+    t0 = time.perf_counter()
+    O.block_covariance(O.expand(imgs, basis))
+    dt = time.perf_counter() - t0
+    return {"value": m / dt, "unit": "images/s", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"first {m} images of {cfg['name']} (oracle: direct Fourier sum + FFT + GL + fp64 covariance), "
+                      f"{dt:.1f} s on the host, numpy/BLAS threads = all cores"}
+
+
+def run_reference(args, cfg, rank):
+    """--impl reference: the fp64 oracle timed as it stands, on a bounded sample per step."""
+    import numpy as np
+    import oracle as O
+    import synth
+    if rank != 0:
+        return
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    sig = synth.blobs.noise_sigma(cfg)
+    m = 4 if cfg["L"] >= 128 else 32
+    imgs = synth.blob_images(cfg, 0, m, sigma_n=sig).double().numpy()
+    for _ in range(args.warmup):
+        O.block_covariance(O.expand(imgs, basis))
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.block_covariance(O.expand(imgs, basis))
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * statistics.median(times)
+    value = m / (ms / 1e3)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg['name']} sample of {m} images (oracle, CPU)", "L": cfg["L"], "R": cfg["R"],
+                       "c": cfg["c"], "n_sample": m},
+            "cpu_baseline": {"value": value, "unit": "images/s", "cores": os.cpu_count(), "kind": "oracle",
+                             "sample": f"{m} images of {cfg['name']} per step"},
+            "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    import synth
+    cfg = synth.config(args.config)
+    if args.n:
+        cfg["n"] = args.n
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1412_0781_b200 as F
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = cfg["n"]
+    s, e = F.shard_range(n, rank, world)
+    n_local = e - s
+    dt = F.F32 if cfg["dtype"] == "f32" else F.F64
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], dtype=dt, device=local, max_batch=4096)
+    comm = None
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            uid = torch.frombuffer(bytearray(F.fbspca_nccl_unique_id()), dtype=torch.uint8).clone()
+        obj = [uid.numpy().tobytes()]
+        dist.broadcast_object_list(obj, src=0)
+        comm = F.fbspca_comm_init(obj[0], world, rank)
+
+    # ---- inputs resident in HBM (generated outside the timed region; shard-invariant generator)
+    sig = synth.blobs.noise_sigma(cfg, device=dev)
+    images = synth.blob_images(cfg, s, n_local, device=dev, sigma_n=sig,
+                               dtype=torch.float32 if dt == F.F32 else torch.float64)
+    coeffs = torch.empty((plan.n_coef, n_local), dtype=plan.complex_dtype, device=dev)
+    blocks = torch.empty(plan.n_blk, dtype=torch.float64, device=dev)
+    mean = torch.empty(int(plan.p[0]), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        F.fbspca_expand(plan, images, coeffs)
+        F.fbspca_covariance(plan, coeffs, n_local, n, comm, blocks, mean)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    F.fbspca_set_timing(plan, True)
+    F.fbspca_get_timing(plan)                     # reset
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    kt = F.fbspca_get_timing(plan)
+    F.fbspca_set_timing(plan, False)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = t.item()
+    value = n / (ms_max / 1e3)
+
+    # ---- e2e: same metric through the public API with HOST (pinned) inputs, H2D inside the timed region,
+    # chunked and double-buffered on a copy stream, plus the D2H of the finalised blocks.
+    e2e = None
+    if not args.no_e2e:
+        host = images.cpu().pin_memory()
+        CH = 8192
+        bufs = [torch.empty((CH, cfg["L"], cfg["L"]), dtype=images.dtype, device=dev) for _ in range(2)]
+        cbufs = [torch.empty((plan.n_coef, CH), dtype=plan.complex_dtype, device=dev) for _ in range(2)]
+        partial = torch.empty(plan.n_partial, dtype=torch.float64, device=dev)
+        hblocks = torch.empty(plan.n_blk, dtype=torch.float64).pin_memory()
+        cstream = torch.cuda.Stream(device=dev)
+        copied = [torch.cuda.Event() for _ in range(2)]
+        consumed = [torch.cuda.Event() for _ in range(2)]
+
+        def e2e_step():
+            partial.zero_()
+            chunks = [(a, min(a + CH, n_local)) for a in range(0, n_local, CH)]
+            for i, (a, b) in enumerate(chunks):
+                j = i & 1
+                with torch.cuda.stream(cstream):
+                    cstream.wait_event(consumed[j])
+                    bufs[j][: b - a].copy_(host[a:b], non_blocking=True)
+                    copied[j].record(cstream)
+                stream.wait_event(copied[j])
+                img = bufs[j][: b - a]
+                co = cbufs[j][:, : b - a] if b - a == CH else torch.empty((plan.n_coef, b - a), dtype=plan.complex_dtype, device=dev)
+                F.fbspca_expand(plan, img, co)
+                F.fbspca_covariance_accumulate(plan, co, partial)
+                consumed[j].record(stream)
+            F.fbspca_allreduce_partial(plan, partial, comm)
+            bl, _ = F.fbspca_covariance_finalize(plan, partial)
+            hblocks.copy_(bl, non_blocking=True)
+
+        for _ in range(min(2, args.warmup)):
+            e2e_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        barrier()
+        te = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": n / (te.item() / 1e3), "unit": "images/s",
+               "h2d_bytes_per_step": int(host.numel() * host.element_size()) * world,
+               "d2h_bytes_per_step": int(hblocks.numel() * 8) * world, "ms_per_step": te.item(),
+               "note": "pinned host images, 8192-image chunks double-buffered on a copy stream; "
+                       "fbspca_expand + fbspca_covariance_accumulate per chunk, all-reduce, finalize, D2H blocks"}
+
+    if rank == 0:
+        pk = peaks()
+        hbm = pk.get("hbm_gbs", 6650.7)
+        wk = work_per_image(plan, cfg["L"])
+        launches = {k: int(v[1]) for k, v in kt.items()}
+        kms = {k: v[0] / args.steps for k, v in kt.items()}
+        # polar kernel: every timed region is one launch
+        per_launch_polar_ms = kt["polar_K1K2K3"][0] / max(1, kt["polar_K1K2K3"][1])
+        imgs_per_launch = n_local / max(1, kt["polar_K1K2K3"][1] / args.steps)
+        sm_max = pk.get("sm_max_mhz", 1965.0)
+        alu_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12          # fp32 FFMA TFLOP/s at max clock
+        achieved = wk["polar_flops"] * imgs_per_launch / (per_launch_polar_ms / 1e3) / 1e12
+        n_cov_launch = math.ceil(n_local / 4096)
+        gpu_launches = args.steps * (2 * math.ceil(n_local / plan_batch(plan)) + n_cov_launch + 1)
+        kernels = {}
+        for name, tms in kms.items():
+            if tms <= 0:
+                continue
+            d = {"ms_per_step": tms, "launches_per_step": launches[name] / args.steps}
+            if name == "polar_K1K2K3":
+                d["tflops"] = wk["polar_flops"] * n_local / (tms / 1e3) / 1e12
+                d["alg_gbs"] = wk["polar_bytes"] * n_local / (tms / 1e3) / 1e9
+            elif name == "radial_K4":
+                d["tflops"] = wk["k4"] * n_local / (tms / 1e3) / 1e12
+                d["alg_gbs"] = wk["radial_bytes"] * n_local / (tms / 1e3) / 1e9
+            elif name == "cov_K5":
+                d["tflops"] = wk["k5"] * n_local / (tms / 1e3) / 1e12
+                d["alg_gbs"] = wk["cov_bytes"] * n_local / (tms / 1e3) / 1e9
+            kernels[name] = d
+        staged = 1.57e6 if cfg["name"] == "C3" else None
+        line = {
+            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32" if dt == F.F32 else "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg['name']}: BASELINE.json configs[{int(cfg['name'][1]) - 1}]", "n": n,
+                       "L": cfg["L"], "R": cfg["R"], "c": cfg["c"], "parallelism": f"dp{world}",
+                       "n_per_rank": n_local, "eps": 1e-5, "M": plan.M, "w": plan.w,
+                       "l2": "inputs larger than L2 (6.5 GB images per step at C3)"},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
+                         "frac": achieved / alu_peak, "traffic": None, "kernel": "polar_K1K2K3",
+                         "peak_source": f"148 SM x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz (guide unit counts, "
+                                        "MEASURED_PEAKS sm_max_mhz)",
+                         "per_image_flops": wk["polar_flops"]},
+            "hbm_roofline": {"staged_min_bytes_per_image": staged, "hbm_gbs_measured": hbm,
+                             "frac_of_staged_roofline": (value / world) / (hbm * 1e9 / staged) if staged else None,
+                             "algorithmic_bytes_per_image": wk["algorithmic_bytes"],
+                             "frac_of_algorithmic_roofline": (value / world) / (hbm * 1e9 / wk["algorithmic_bytes"])},
+            "kernels": kernels,
+            "clocks": clk,
+            "gpu_launches": gpu_launches,
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = cpu_baseline(cfg)
+            except Exception as ex:  # the baseline is reported, never the target
+                line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
+        print(json.dumps(line), flush=True)
+    if comm:
+        F.fbspca_comm_destroy(comm)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
+def plan_batch(plan):
+    return 4096
+
+
+if __name__ == "__main__":
+    main()

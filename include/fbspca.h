@@ -1,0 +1,156 @@
+/*
+ * fbspca.h -- C ABI of the B200 (sm_100a) Fast Fourier-Bessel steerable PCA hot path.
+ *
+ * Method: Zhao, Shkolnisky, Singer, "Fast Steerable Principal Component Analysis"
+ * (arXiv 1412.0781).  "P:n" cites line n of that paper's text.
+ *
+ *   Algorithm 1  fbspca_expand      images -> FB coefficients a_{k,q}
+ *   Algorithm 2  fbspca_covariance  C^(k) = Re(A_k A_k^*)/n, mean at k=0 only
+ *                            fbspca_eig         C^(k) = U_k diag(lambda^(k)) U_k^T
+ *                            fbspca_project     c^i_{k,l} = sum_q a^i_{k,q} u_l^(k)(q) (+ filter)
+ *
+ * Conventions (all fixed):
+ *   - images: n x L x L, row-major, axis 0 = i1 (multiplies xi_1 = xi cos theta),
+ *     pixel a <-> i = a - floor(L/2)  (reading Q3).
+ *   - Fourier sum with unit prefactor: F(I)(xi) = sum_i I(i) e^{-2 pi i xi.i}  (Eq. (nufft), reading Q1).
+ *   - coefficients ("coefficient layout"): complex, k-major.  Block k (k = 0..k_max) is a p_k x ld matrix
+ *     starting at complex element coef_off[k]*ld, row q (q = 0..p_k-1, the paper's q-1), column = image,
+ *     images contiguous, re/im interleaved.  ld = the number of images of the call (n or n_local).
+ *     k = 0 has Im = 0 (reading Q8).  Only k >= 0 is stored: a_{-k,q} = conj(a_{k,q}).
+ *   - covariance blocks ("packed layout", fp64): for each k the upper triangle of C^(k), row-major over
+ *     q <= q', starting at blk_off[k]; total blk_off[k_max+1].
+ *   - eigenpairs (fp64): evals at coef_off[k] + l (descending per k), evecs U_k row-major p_k x p_k at
+ *     evec_off[k] (element [q][l] = u_l^(k)(q)); sign: largest-|u| entry positive (reading Q10).
+ *
+ * Ownership: every pointer argument except the plan is owned by the caller.  "d_" pointers are device
+ * pointers on the plan's device; all calls are asynchronous on the given stream unless stated, and a plan
+ * must not be used concurrently from two streams.  The plan owns its tables and a workspace sized by
+ * max_batch; no call allocates device memory.
+ *
+ * Errors: every call returns fbspca_status; fbspca_last_error() returns a thread-local message.
+ */
+#ifndef FBSPCA_H
+#define FBSPCA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fbspca_plan_s* fbspca_plan_t;   /* opaque */
+typedef void* fbspca_stream_t;                 /* a cudaStream_t (NULL = legacy default stream) */
+
+typedef enum {
+  FBSPCA_OK = 0,
+  FBSPCA_ERR_ARG = 1,      /* null/misaligned pointer, n < 1, n_total < n_local, bad mode        */
+  FBSPCA_ERR_CONFIG = 2,   /* c not in (0, 1/2], R < 2 or cR < 1, R > L/2, eps out of range, ...   */
+  FBSPCA_ERR_CUDA = 3,     /* a CUDA runtime error (message carries cudaGetErrorString)           */
+  FBSPCA_ERR_NCCL = 4,     /* NCCL missing or failed                                             */
+  FBSPCA_ERR_NUMERIC = 5   /* Jacobi did not converge (message names k)                           */
+} fbspca_status;
+
+typedef enum { FBSPCA_F32 = 0, FBSPCA_F64 = 1 } fbspca_dtype;
+
+/* Build a plan (Alg. 1 lines 1-2): census R_{k,q+1} <= 2 pi c R (Eq. (criterion1)),
+ * n_xi = ceil(4cR), n_theta = ceil(16cR), Gauss-Legendre nodes on [0,c], the radial
+ * table N_{k,q} J_k(R_{k,q} xi_j/c) xi_j w_j (2 pi/n_theta) (Eq. (a) P:195 with the 1/n_theta of
+ * Eq. (1DFFT) P:189 folded in), and the NUFFT window (width from eps) and deapodisation.
+ *   L        image side (>= 4).  c band limit in (0, 1/2].  R support radius, 2 <= R <= L/2, cR >= 1.
+ *   eps      NUFFT accuracy target (relative l2 of the polar samples), [1e-14, 1e-3]; <= 0 picks the
+ *            default (1e-5 for F32, 1e-12 for F64).  F32 rejects eps < 1e-6.
+ *   dt       FBSPCA_F32: images float, coefficients complex64.  FBSPCA_F64: double / complex128.
+ *   device   CUDA device ordinal, or -1 for a host-only plan (census/tables only; every compute call
+ *            on it returns FBSPCA_ERR_ARG).  Synchronous.
+ *   max_batch  images per internal batch (workspace size); <= 0 picks 4096. */
+fbspca_status fbspca_plan(int L, double c, double R, double eps, fbspca_dtype dt, int device,
+                          int64_t max_batch, fbspca_plan_t* out);
+
+/* Read-only views into the plan (valid until fbspca_destroy).  Any output pointer may be NULL.
+ *   p_k[k_max+1]; coef_off[k_max+2] (coef_off[k_max+1] = sum p_k); blk_off[k_max+2] (packed fp64
+ *   covariance; blk_off[k_max+1] = total); evec_off[k_max+2]. */
+fbspca_status fbspca_plan_info(fbspca_plan_t plan, int* n_xi, int* n_theta, int* k_max,
+                               const int** p_k, const int64_t** coef_off, const int64_t** blk_off,
+                               const int64_t** evec_off);
+
+/* Extra plan facts: NUFFT oversampled grid M, window width w, kernel shape beta, number of column
+ * phases of the fused polar kernel, its dynamic shared memory bytes, and the census zeros R_{k,q}
+ * (host array, q = 1..p_k, laid out like coef_off) and GL nodes/weights (host, n_xi each). */
+fbspca_status fbspca_plan_detail(fbspca_plan_t plan, int* M, int* w, double* beta, int* n_phase,
+                                 int* smem_bytes, const double** zeros, const double** xi,
+                                 const double** wq);
+
+/* Alg. 1 lines 3-4: a = T* I for n images.  NUFFT (K1 pad+deapodise+2-D FFT, K2 window gather
+ * to the half-plane polar nodes), K3 angular FFT (Eq. (1DFFT)), K4 radial quadrature (Eq. (a)).
+ *   d_images  n x L x L (float or double per dt), device.   d_coeffs  sum_k p_k x n complex (coefficient
+ *   layout, ld = n), device.  Streams any n in batches of max_batch. */
+fbspca_status fbspca_expand(fbspca_plan_t plan, const void* d_images, int64_t n, void* d_coeffs,
+                            fbspca_stream_t stream);
+
+/* Alg. 2 lines 1-4, data-parallel form: K5 accumulates, over this rank's n_local
+ * coefficient columns, S_k = sum_i Re(a_k a_k^*) (packed), s_0 = sum_i a_{0,i} and the count; then, if
+ * nccl_comm != NULL, ONE in-place ncclAllReduce(sum, fp64) of that buffer across ranks; then finalises
+ *   C^(0) = S_0/n - s_0 s_0^T / n^2   (= (1/n) sum (a_0 - m)(a_0 - m)^T, Eq. (ck_0) P:348 after P:394),
+ *   C^(k) = S_k / n                   (Eq. (ck)),     m = s_0 / n,
+ * with n the all-reduced count (= n_total).  d_coeffs: coefficient layout with ld = n_local.
+ * d_blocks: blk_off[k_max+1] doubles (packed, finalised).  d_mean: p_0 doubles.  nccl_comm: an ncclComm_t
+ * from fbspca_comm_init, or NULL for one GPU. */
+fbspca_status fbspca_covariance(fbspca_plan_t plan, const void* d_coeffs, int64_t n_local,
+                                int64_t n_total, void* nccl_comm, double* d_blocks, double* d_mean,
+                                fbspca_stream_t stream);
+
+/* Same as fbspca_covariance but stops before the all-reduce: writes the un-finalised partial buffer
+ * (packed S_k, then s_0 (p_0 doubles), then the count) to d_partial (blk_off[k_max+1] + p_0 + 1 doubles).
+ * fbspca_covariance_finalize turns a (reduced) partial buffer into blocks and mean. */
+fbspca_status fbspca_covariance_partial(fbspca_plan_t plan, const void* d_coeffs, int64_t n_local,
+                                        double* d_partial, fbspca_stream_t stream);
+fbspca_status fbspca_covariance_finalize(fbspca_plan_t plan, const double* d_partial, double* d_blocks,
+                                         double* d_mean, fbspca_stream_t stream);
+
+/* Streaming form: like fbspca_covariance_partial but ADDS this call's n_local columns into an existing
+ * partial buffer (zero it once with cudaMemset or a first fbspca_covariance_partial).  Lets a caller
+ * expand and accumulate a stack chunk by chunk (e.g. overlapping host->device copies with compute). */
+fbspca_status fbspca_covariance_accumulate(fbspca_plan_t plan, const void* d_coeffs, int64_t n_local,
+                                           double* d_partial, fbspca_stream_t stream);
+
+/* In-place ncclAllReduce(sum, fp64) of a partial buffer over nccl_comm (no-op when nccl_comm == NULL). */
+fbspca_status fbspca_allreduce_partial(fbspca_plan_t plan, double* d_partial, void* nccl_comm,
+                                       fbspca_stream_t stream);
+
+/* Alg. 2 line 4: batched cyclic (parallel-ordered) Jacobi in fp64, one block per CTA.
+ * d_blocks packed (input), d_evals (coef_off[k_max+1] doubles), d_evecs (evec_off[k_max+1] doubles).
+ * Synchronises the stream to check convergence (<= 30 sweeps); FBSPCA_ERR_NUMERIC names the block. */
+fbspca_status fbspca_eig(fbspca_plan_t plan, const double* d_blocks, double* d_evals, double* d_evecs,
+                         fbspca_stream_t stream);
+
+/* Alg. 2 line 6 (Eq. (sPCAcoeff)) with optional filtering:
+ *   out_k[l][i] = h^(k)_l sum_q u_l^(k)(q) (a^i_{k,q} - [k=0] m_q)
+ *   mode 0: h = 1.   mode 1: Eq. (compselect) lambda > sigma2 (1 + sqrt(gamma_k))^2 (gamma_0 = p_0/n_total,
+ *   gamma_k = p_k/(2 n_total)), then h = l/(l + sigma2), l = (lambda - sigma2)_+ (reading Q13), else 0.
+ *   mode 2: as 1 with the spiked-model l.
+ * d_coeffs / d_out: coefficient layout with ld = n (d_out may not alias d_coeffs). */
+fbspca_status fbspca_project(fbspca_plan_t plan, const void* d_coeffs, int64_t n, const double* d_mean,
+                             const double* d_evals, const double* d_evecs, double sigma2, int mode,
+                             int64_t n_total, void* d_out, fbspca_stream_t stream);
+
+/* NCCL plumbing (libnccl.so.2 is dlopen'ed on first use).  unique_id: 128 bytes. */
+fbspca_status fbspca_nccl_unique_id(void* unique_id_out);
+fbspca_status fbspca_comm_init(const void* unique_id, int nranks, int rank, void** nccl_comm_out);
+fbspca_status fbspca_comm_destroy(void* nccl_comm);
+
+/* Per-kernel-family device times when timing is on (CUDA events recorded around each launch on the
+ * call's stream; off by default).  fbspca_get_timing synchronises those events, returns *count family
+ * names, ms[0..count) = summed milliseconds and ms[count..2*count) = number of timed launch regions since
+ * the previous fbspca_get_timing, then resets the accumulators. */
+fbspca_status fbspca_set_timing(fbspca_plan_t plan, int enabled);
+fbspca_status fbspca_get_timing(fbspca_plan_t plan, int* count, const char* const** names,
+                                const float** ms);
+
+void fbspca_destroy(fbspca_plan_t plan);
+const char* fbspca_last_error(void);
+const char* fbspca_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FBSPCA_H */

@@ -1,0 +1,129 @@
+// internal.h -- plan structure shared by the host plan builder, the C-ABI layer and the kernels.
+// Nothing here is visible through include/fbspca.h.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/fbspca.h"
+
+namespace fbspca {
+
+constexpr int kMaxRadixStages = 16;
+constexpr int kMaxPhases = 64;
+
+// Stockham radix plan for a length-N FFT (N = prod radices; radices in {2,3,4,5,8}).
+struct FftPlan {
+  int n = 0;
+  int nstages = 0;
+  int radix[kMaxRadixStages] = {0};
+};
+
+// Everything a polar-kernel launch needs, passed by value (fits the 32 KB param space).
+struct PolarParams {
+  int L, M, w, n_xi, n_theta, half, k_max;
+  int col_lo, ncols_x;            // X scratch columns cover m2 in [col_lo, col_lo + ncols_x)
+  int S;                          // phase chunk width (columns) and its padded row stride
+  int n_phase;
+  int phase_lo[kMaxPhases];       // first column (m2) of phase p
+  int phase_node_begin[kMaxPhases + 1];
+  double beta;
+  double half_w;                  // w/2
+  int nwarps;
+  int ring_group;                 // rings staged together in the angular pass
+  int smem_region_bytes;          // bytes of the shared work region (complex units * sizeof)
+  FftPlan fft_M, fft_theta;
+  // device pointers (plan-owned)
+  const void* deapod;             // L values (T): d(i) = 1/Phi(i/M), i = a - floor(L/2)
+  const void* tw_M;               // M complex (T2): e^{-2 pi i t / M}
+  const void* tw_theta;           // n_theta complex (T2)
+  const double* rho;              // n_xi: xi_j * M
+  const double* cs;               // half x 2: cos(theta_l), sin(theta_l)
+  const uint32_t* nodes;          // (j << 16) | l, grouped by phase
+  void* xscratch;                 // per resident CTA: L x ncols_x complex
+  void* pscratch;                 // per resident CTA: n_xi x half complex
+  int64_t xscratch_stride, pscratch_stride;   // complex elements per CTA
+};
+
+struct Plan {
+  // configuration
+  int L = 0;
+  double c = 0, R = 0, eps = 0;
+  fbspca_dtype dt = FBSPCA_F32;
+  int device = -1;
+  int64_t max_batch = 0;
+  // census
+  int k_max = -1;
+  std::vector<int> p;                    // p_k
+  std::vector<int64_t> coef_off;         // k_max+2
+  std::vector<int64_t> blk_off;          // k_max+2 (packed upper triangles)
+  std::vector<int64_t> evec_off;         // k_max+2 (p_k^2)
+  std::vector<double> zeros;             // R_{k,q}, coef_off layout
+  std::vector<double> norm;              // N_{k,q}
+  // quadrature grid
+  int n_xi = 0, n_theta = 0;
+  std::vector<double> xi, wq;
+  std::vector<double> table;             // [coef row][j]: N J_k(R xi_j/c) xi_j w_j (2 pi / n_theta)
+  // NUFFT
+  int M = 0, w = 0;
+  double beta = 0;
+  std::vector<double> deapod;            // L
+  std::vector<double> rho, cs;           // xi_j M; (cos, sin)(theta_l), l < n_theta/2
+  PolarParams pp{};                      // host copy (device pointers filled at upload)
+  std::vector<uint32_t> nodes;
+  int polar_smem = 0;
+  int polar_grid = 0;                    // resident CTAs of the polar kernel
+  // device buffers
+  void* d_table = nullptr;               // T (float or double), coef rows x n_xi
+  void* d_deapod = nullptr;
+  void* d_tw_M = nullptr;
+  void* d_tw_theta = nullptr;
+  double* d_rho = nullptr;
+  double* d_cs = nullptr;
+  uint32_t* d_nodes = nullptr;
+  PolarParams* d_pp = nullptr;           // device copy of pp
+  void* d_xscratch = nullptr;
+  void* d_pscratch = nullptr;
+  void* d_ghat = nullptr;                // (k_max+1) x max_batch x 2 x n_xi  (T)
+  double* d_partial = nullptr;           // blk_off[k_max+1] + p_0 + 1
+  int* d_coef_k = nullptr;               // row -> k lookup (coef rows)
+  int* d_p = nullptr;
+  int64_t* d_coef_off = nullptr;
+  int64_t* d_blk_off = nullptr;
+  int64_t* d_evec_off = nullptr;
+  double* d_eig_work = nullptr;          // 2 * evec_off[k_max+1]
+  int* d_eig_sweeps = nullptr;           // k_max+1
+  // timing
+  bool timing = false;
+  std::vector<std::string> tnames;
+  std::vector<const char*> tname_ptrs;
+  std::vector<float> tms;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> tevents;
+  int num_sms = 0;
+};
+
+// ---- host plan construction (plan.cpp) ----
+fbspca_status build_host_plan(Plan& P);           // census, grid, table, NUFFT, phases (no CUDA)
+void set_error(const std::string& msg);
+
+// ---- launchers (kernels_*.cu) ----
+cudaError_t launch_polar(const Plan& P, const void* d_images, int64_t n_img, int64_t img_stride_elems,
+                         cudaStream_t s);
+cudaError_t launch_radial(const Plan& P, int64_t nb, int64_t i0, int64_t ld, void* d_coeffs,
+                          cudaStream_t s);
+cudaError_t launch_cov_accum(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb,
+                             double* d_partial, cudaStream_t s);
+cudaError_t launch_cov_finalize(const Plan& P, const double* d_partial, double* d_blocks, double* d_mean,
+                                cudaStream_t s);
+cudaError_t launch_eig(const Plan& P, const double* d_blocks, double* d_evals, double* d_evecs,
+                       cudaStream_t s);
+cudaError_t launch_project(const Plan& P, const void* d_coeffs, int64_t n, const double* d_mean,
+                           const double* d_evals, const double* d_evecs, double sigma2, int mode,
+                           int64_t n_total, void* d_out, cudaStream_t s);
+int polar_max_smem();
+int fft_values_per_lane(const FftPlan& f);
+int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps);
+
+}  // namespace fbspca

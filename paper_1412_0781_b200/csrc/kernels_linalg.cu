@@ -1,0 +1,409 @@
+// kernels_linalg.cu -- K4 radial quadrature, K5 covariance accumulation + finalise, K6 batched Jacobi,
+// K7 projection / filtering.  SIMT versions (fp32 FFMA with fp64 accumulation across batches).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "internal.h"
+
+namespace fbspca {
+
+// ---------------------------------------------------------------- K4: Eq. (a)
+// For block k:  D[row][q] = sum_j ghat[k][row][j] * T[coef_off[k] + q][j],  row = 2 b + part (re/im),
+// written to coeffs (real view) at [(coef_off[k] + q) * 2 ld + 2 i0 + row].  Im of k = 0 set to 0 (Q8).
+template <typename T>
+__global__ void __launch_bounds__(256)
+radial_kernel(const T* __restrict__ ghat, const T* __restrict__ table, const int* __restrict__ p,
+              const int64_t* __restrict__ coef_off, int nb, int n_xi, int64_t i0, int64_t ld,
+              T* __restrict__ out) {
+  constexpr int BM = 64, BN = 64, BK = 32;
+  __shared__ T As[BK][BM + 1];
+  __shared__ T Bs[BK][BN + 1];
+  const int k = blockIdx.y;
+  const int pk = p[k];
+  const int q0 = blockIdx.z * BN;
+  if (q0 >= pk) return;
+  const int rows = 2 * nb;
+  const int r0 = blockIdx.x * BM;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const T* A = ghat + (int64_t)k * rows * n_xi;
+  const T* B = table + coef_off[k] * n_xi;
+  T acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+  for (int j0 = 0; j0 < n_xi; j0 += BK) {
+    for (int e = tid; e < BM * BK; e += 256) {
+      const int rr = e / BK, jj = e - rr * BK;
+      const int r = r0 + rr, j = j0 + jj;
+      As[jj][rr] = (r < rows && j < n_xi) ? A[(int64_t)r * n_xi + j] : T(0);
+      const int q = q0 + rr;
+      Bs[jj][rr] = (q < pk && j < n_xi) ? B[(int64_t)q * n_xi + j] : T(0);
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < BK; ++kk) {
+      T a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { a[i] = As[kk][tx + 16 * i]; b[i] = Bs[kk][ty + 16 * i]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
+    }
+    __syncthreads();
+  }
+  const int64_t base = coef_off[k];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int q = q0 + ty + 16 * j;
+    if (q >= pk) continue;
+    T* o = out + (base + q) * 2 * ld + 2 * i0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = r0 + tx + 16 * i;
+      if (r < rows) o[r] = (k == 0 && (r & 1)) ? T(0) : acc[i][j];
+    }
+  }
+}
+
+cudaError_t launch_radial(const Plan& P, int64_t nb, int64_t i0, int64_t ld, void* d_coeffs, cudaStream_t s) {
+  int pmax = P.p[0];
+  dim3 grid((unsigned)((2 * nb + 63) / 64), (unsigned)(P.k_max + 1), (unsigned)((pmax + 63) / 64));
+  if (P.dt == FBSPCA_F32)
+    radial_kernel<float><<<grid, 256, 0, s>>>((const float*)P.d_ghat, (const float*)P.d_table, P.d_p, P.d_coef_off,
+                                              (int)nb, P.n_xi, i0, ld, (float*)d_coeffs);
+  else
+    radial_kernel<double><<<grid, 256, 0, s>>>((const double*)P.d_ghat, (const double*)P.d_table, P.d_p,
+                                               P.d_coef_off, (int)nb, P.n_xi, i0, ld, (double*)d_coeffs);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K5: Eqs. (ck), (ck_0)
+// partial[blk_off[k] + packed(q, q')] += sum_{c in batch} A_k[q][c] A_k[q'][c]   (q <= q')
+// where A_k is the real view (re/im interleaved along images) of block k: sum over re and im gives
+// Re(a a^*).  k = 0 accumulates in fp64 (reading F9) and also s_0 and the count.
+__device__ __forceinline__ int64_t packed_idx(int q, int qq, int p) {
+  return (int64_t)q * p - (int64_t)q * (q - 1) / 2 + (qq - q);
+}
+
+template <typename T, typename Acc>
+__device__ void cov_tile(const T* __restrict__ Ak, int pk, int64_t ld2, int64_t c0, int64_t ncol, int tq, int tqq,
+                         double* __restrict__ dst, T (*S1)[64 + 1], T (*S2)[64 + 1]) {
+  constexpr int BK = 32;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int qa = tq * 64, qb = tqq * 64;
+  Acc acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = Acc(0);
+  for (int64_t cb = 0; cb < ncol; cb += BK) {
+    for (int e = tid; e < 64 * BK; e += 256) {
+      const int rr = e / BK, cc = e - rr * BK;
+      const int64_t c = cb + cc;
+      const int q1 = qa + rr, q2 = qb + rr;
+      S1[cc][rr] = (q1 < pk && c < ncol) ? Ak[(int64_t)q1 * ld2 + c0 + c] : T(0);
+      S2[cc][rr] = (q2 < pk && c < ncol) ? Ak[(int64_t)q2 * ld2 + c0 + c] : T(0);
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < BK; ++kk) {
+      Acc a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { a[i] = Acc(S1[kk][tx + 16 * i]); b[i] = Acc(S2[kk][ty + 16 * i]); }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int q = qa + tx + 16 * i, qq = qb + ty + 16 * j;
+      if (q < pk && qq < pk && q <= qq) dst[packed_idx(q, qq, pk)] += double(acc[i][j]);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+cov_accum_kernel(const T* __restrict__ coeffs, const int* __restrict__ p, const int64_t* __restrict__ coef_off,
+                 const int64_t* __restrict__ blk_off, int64_t ld, int64_t i0, int64_t nb, int k_max,
+                 double* __restrict__ partial) {
+  __shared__ T S1[32][64 + 1];
+  __shared__ T S2[32][64 + 1];
+  const int k = blockIdx.x;
+  const int pk = p[k];
+  const int nt = (pk + 63) / 64;
+  int pair = blockIdx.y, tq = 0;
+  while (tq < nt && pair >= nt - tq) { pair -= nt - tq; ++tq; }
+  if (tq >= nt) return;
+  const int tqq = tq + pair;
+  const T* Ak = coeffs + coef_off[k] * 2 * ld;
+  double* dst = partial + blk_off[k];
+  if (k == 0)
+    cov_tile<T, double>(Ak, pk, 2 * ld, 2 * i0, 2 * nb, tq, tqq, dst, S1, S2);
+  else
+    cov_tile<T, T>(Ak, pk, 2 * ld, 2 * i0, 2 * nb, tq, tqq, dst, S1, S2);
+  if (k == 0 && blockIdx.y == 0) {
+    double* s0 = partial + blk_off[k_max + 1];
+    for (int q = threadIdx.x; q < pk; q += blockDim.x) {
+      double s = 0;
+      const T* row = Ak + (int64_t)q * 2 * ld + 2 * i0;
+      for (int64_t c = 0; c < nb; ++c) s += double(row[2 * c]);
+      s0[q] += s;
+    }
+    if (threadIdx.x == 0) s0[pk] += double(nb);
+  }
+}
+
+cudaError_t launch_cov_accum(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb,
+                             double* d_partial, cudaStream_t s) {
+  const int nt = (P.p[0] + 63) / 64;
+  dim3 grid((unsigned)(P.k_max + 1), (unsigned)(nt * (nt + 1) / 2));
+  if (P.dt == FBSPCA_F32)
+    cov_accum_kernel<float><<<grid, 256, 0, s>>>((const float*)d_coeffs, P.d_p, P.d_coef_off, P.d_blk_off, ld, i0, nb,
+                                                 P.k_max, d_partial);
+  else
+    cov_accum_kernel<double><<<grid, 256, 0, s>>>((const double*)d_coeffs, P.d_p, P.d_coef_off, P.d_blk_off, ld, i0,
+                                                  nb, P.k_max, d_partial);
+  return cudaGetLastError();
+}
+
+// C^(0) = S_0/n - s0 s0^T/n^2, C^(k) = S_k/n, mean = s0/n   (n = all-reduced count)
+__global__ void cov_finalize_kernel(const double* __restrict__ partial, const int* __restrict__ p,
+                                    const int64_t* __restrict__ blk_off, int k_max, double* __restrict__ blocks,
+                                    double* __restrict__ mean) {
+  const int k = blockIdx.y;
+  const int pk = p[k];
+  const int64_t tot = blk_off[k_max + 1];
+  const double* s0 = partial + tot;
+  const double n = s0[p[0]];
+  const int64_t npk = (int64_t)pk * (pk + 1) / 2;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < npk; idx += (int64_t)gridDim.x * blockDim.x) {
+    double v = partial[blk_off[k] + idx] / n;
+    if (k == 0) {
+      int q = 0;
+      while (q + 1 < pk && packed_idx(q + 1, q + 1, pk) <= idx) ++q;
+      const int qq = q + int(idx - packed_idx(q, q, pk));
+      v -= (s0[q] / n) * (s0[qq] / n);
+    }
+    blocks[blk_off[k] + idx] = v;
+  }
+  if (k == 0 && blockIdx.x == 0)
+    for (int q = threadIdx.x; q < pk; q += blockDim.x) mean[q] = s0[q] / n;
+}
+
+cudaError_t launch_cov_finalize(const Plan& P, const double* d_partial, double* d_blocks, double* d_mean,
+                                cudaStream_t s) {
+  const int64_t maxp = (int64_t)P.p[0] * (P.p[0] + 1) / 2;
+  dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((maxp + 255) / 256, 64)), (unsigned)(P.k_max + 1));
+  cov_finalize_kernel<<<grid, 256, 0, s>>>(d_partial, P.d_p, P.d_blk_off, P.k_max, d_blocks, d_mean);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K6: batched parallel-order Jacobi
+// One CTA per block.  Round-robin pairing (p' = p rounded up to even; p'/2 disjoint pairs per round,
+// p'-1 rounds per sweep); rotations from Golub-Van Loan sym.schur2, applied as A <- J^T A J, V <- V J.
+constexpr int kEigMaxSmemA = 144 * 144;   // doubles of A kept in shared memory
+
+__global__ void __launch_bounds__(256)
+eig_kernel(const double* __restrict__ blocks, const int* __restrict__ p, const int64_t* __restrict__ blk_off,
+           const int64_t* __restrict__ coef_off, const int64_t* __restrict__ evec_off, double* __restrict__ evals,
+           double* __restrict__ evecs, double* __restrict__ work, int* __restrict__ sweeps_out) {
+  extern __shared__ double sh[];
+  const int k = blockIdx.x;
+  const int n = p[k];
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  double* cs_c = sh;                 // pairs
+  double* cs_s = sh + 128;
+  int* pi = reinterpret_cast<int*>(sh + 256);
+  int* qi = pi + 128;
+  double* red = sh + 384;            // reduction scratch (nthr)
+  double* A = (n * n <= kEigMaxSmemA) ? (sh + 384 + 256) : (work + 2 * evec_off[k]);
+  double* V = work + 2 * evec_off[k] + (int64_t)n * n;
+  const double* Bk = blocks + blk_off[k];
+  for (int idx = tid; idx < n * n; idx += nthr) {
+    const int r = idx / n, c = idx - r * n;
+    const int q = min(r, c), qq = max(r, c);
+    A[idx] = Bk[packed_idx(q, qq, n)];
+    V[idx] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int np = n + (n & 1), npairs = np / 2;
+  int sweep = 0;
+  for (; sweep < 30 && n > 1; ++sweep) {
+    double off = 0, dg = 0;
+    for (int idx = tid; idx < n * n; idx += nthr) {
+      const int r = idx / n, c = idx - r * n;
+      const double v = A[idx] * A[idx];
+      if (r == c) dg += v; else off += v;
+    }
+    red[tid] = off; __syncthreads();
+    for (int st = nthr / 2; st > 0; st >>= 1) { if (tid < st) red[tid] += red[tid + st]; __syncthreads(); }
+    off = red[0]; __syncthreads();
+    red[tid] = dg; __syncthreads();
+    for (int st = nthr / 2; st > 0; st >>= 1) { if (tid < st) red[tid] += red[tid + st]; __syncthreads(); }
+    dg = red[0]; __syncthreads();
+    if (off <= 1e-30 * dg || off == 0.0) break;
+    for (int round = 0; round < np - 1; ++round) {
+      for (int i = tid; i < npairs; i += nthr) {
+        auto pos = [&](int t) { return t == 0 ? 0 : 1 + (t - 1 + round) % (np - 1); };
+        int a = pos(i), b = pos(np - 1 - i);
+        int pp = min(a, b), qq = max(a, b);
+        double c = 1, s = 0;
+        if (qq < n) {
+          const double apq = A[pp * n + qq];
+          const double app = A[pp * n + pp], aqq = A[qq * n + qq];
+          if (fabs(apq) > 1e-300 && fabs(apq) > 1e-18 * sqrt(fabs(app * aqq))) {
+            const double tau = (aqq - app) / (2 * apq);
+            const double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1 + tau * tau));
+            c = 1 / sqrt(1 + t * t); s = t * c;
+          }
+        } else { pp = -1; }
+        pi[i] = pp; qi[i] = qq; cs_c[i] = c; cs_s[i] = s;
+      }
+      __syncthreads();
+      // columns: A <- A J, V <- V J
+      for (int idx = tid; idx < npairs * n; idx += nthr) {
+        const int i = idx / n, r = idx - i * n;
+        const int pp = pi[i];
+        if (pp < 0 || cs_s[i] == 0.0) continue;
+        const int qq = qi[i];
+        const double c = cs_c[i], s = cs_s[i];
+        double x = A[r * n + pp], y = A[r * n + qq];
+        A[r * n + pp] = c * x - s * y; A[r * n + qq] = s * x + c * y;
+        x = V[r * n + pp]; y = V[r * n + qq];
+        V[r * n + pp] = c * x - s * y; V[r * n + qq] = s * x + c * y;
+      }
+      __syncthreads();
+      // rows: A <- J^T A
+      for (int idx = tid; idx < npairs * n; idx += nthr) {
+        const int i = idx / n, col = idx - i * n;
+        const int pp = pi[i];
+        if (pp < 0 || cs_s[i] == 0.0) continue;
+        const int qq = qi[i];
+        const double c = cs_c[i], s = cs_s[i];
+        const double x = A[pp * n + col], y = A[qq * n + col];
+        A[pp * n + col] = c * x - s * y; A[qq * n + col] = s * x + c * y;
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) sweeps_out[k] = (n > 1) ? sweep : 0;
+  // sort descending (ties: lower index first) and normalise signs (largest |u| positive, ties lowest q)
+  for (int i = tid; i < n; i += nthr) {
+    const double li = A[i * n + i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double lj = A[j * n + j];
+      rank += (lj > li) || (lj == li && j < i);
+    }
+    evals[coef_off[k] + rank] = li;
+    int arg = 0; double best = -1;
+    for (int r = 0; r < n; ++r) { const double a = fabs(V[r * n + i]); if (a > best) { best = a; arg = r; } }
+    const double sg = V[arg * n + i] < 0 ? -1.0 : 1.0;
+    double* U = evecs + evec_off[k];
+    for (int r = 0; r < n; ++r) U[r * n + rank] = sg * V[r * n + i];
+  }
+}
+
+cudaError_t launch_eig(const Plan& P, const double* d_blocks, double* d_evals, double* d_evecs, cudaStream_t s) {
+  const int pmax = P.p[0];
+  const int an = std::min(pmax * pmax, kEigMaxSmemA);
+  const size_t smem = (384 + 256 + an) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  eig_kernel<<<P.k_max + 1, 256, smem, s>>>(d_blocks, P.d_p, P.d_blk_off, P.d_coef_off, P.d_evec_off, d_evals,
+                                            d_evecs, P.d_eig_work, P.d_eig_sweeps);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K7: Eq. (sPCAcoeff) P:364 + filter P:689-699
+template <typename T>
+__global__ void __launch_bounds__(256)
+project_kernel(const T* __restrict__ coeffs, int64_t n, const double* __restrict__ mean,
+               const double* __restrict__ evals, const double* __restrict__ evecs, const int* __restrict__ p,
+               const int64_t* __restrict__ coef_off, const int64_t* __restrict__ evec_off, double sigma2, int mode,
+               int64_t n_total, T* __restrict__ out) {
+  extern __shared__ unsigned char sm_raw[];
+  const int k = blockIdx.y;
+  const int pk = p[k];
+  T* U = reinterpret_cast<T*>(sm_raw);            // pk x pk
+  T* h = U + pk * pk;                              // pk
+  T* um = h + pk;                                  // pk: U^T mean (k = 0)
+  const double* Uk = evecs + evec_off[k];
+  for (int i = threadIdx.x; i < pk * pk; i += blockDim.x) U[i] = T(Uk[i]);
+  for (int l = threadIdx.x; l < pk; l += blockDim.x) {
+    const double lam = evals[coef_off[k] + l];
+    double hv = 1.0;
+    if (mode != 0) {
+      const double g = (k == 0) ? double(pk) / double(n_total) : double(pk) / (2.0 * double(n_total));
+      const double edge = sigma2 * (1 + sqrt(g)) * (1 + sqrt(g));
+      double ell;
+      if (mode == 1) ell = fmax(lam - sigma2, 0.0);
+      else {
+        const double t = lam - sigma2 * (1 + g);
+        ell = 0.5 * (t + sqrt(fmax(t * t - 4 * g * sigma2 * sigma2, 0.0)));
+      }
+      hv = (lam > edge) ? (sigma2 > 0 ? ell / (ell + sigma2) : 1.0) : 0.0;
+    }
+    h[l] = T(hv);
+    double s = 0;
+    if (k == 0) for (int q = 0; q < pk; ++q) s += Uk[q * pk + l] * mean[q];
+    um[l] = T(s);
+  }
+  __syncthreads();
+  const int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (col >= 2 * n) return;
+  const bool re = (col & 1) == 0;
+  const T* a = coeffs + coef_off[k] * 2 * n + col;
+  T* o = out + coef_off[k] * 2 * n + col;
+  constexpr int LC = 16;
+  for (int l0 = 0; l0 < pk; l0 += LC) {
+    T acc[LC];
+#pragma unroll
+    for (int t = 0; t < LC; ++t) acc[t] = T(0);
+    for (int q = 0; q < pk; ++q) {
+      const T v = a[(int64_t)q * 2 * n];
+#pragma unroll
+      for (int t = 0; t < LC; ++t) if (l0 + t < pk) acc[t] += U[q * pk + l0 + t] * v;
+    }
+#pragma unroll
+    for (int t = 0; t < LC; ++t) {
+      const int l = l0 + t;
+      if (l < pk) {
+        T v = acc[t];
+        if (k == 0) v = re ? v - um[l] : T(0);
+        o[(int64_t)l * 2 * n] = h[l] * v;
+      }
+    }
+  }
+}
+
+cudaError_t launch_project(const Plan& P, const void* d_coeffs, int64_t n, const double* d_mean,
+                           const double* d_evals, const double* d_evecs, double sigma2, int mode, int64_t n_total,
+                           void* d_out, cudaStream_t s) {
+  const int pmax = P.p[0];
+  dim3 grid((unsigned)((2 * n + 255) / 256), (unsigned)(P.k_max + 1));
+  if (P.dt == FBSPCA_F32) {
+    const size_t smem = (size_t)(pmax * pmax + 2 * pmax) * sizeof(float);
+    cudaError_t e = cudaFuncSetAttribute(project_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    project_kernel<float><<<grid, 256, smem, s>>>((const float*)d_coeffs, n, d_mean, d_evals, d_evecs, P.d_p,
+                                                  P.d_coef_off, P.d_evec_off, sigma2, mode, n_total, (float*)d_out);
+  } else {
+    const size_t smem = (size_t)(pmax * pmax + 2 * pmax) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(project_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    project_kernel<double><<<grid, 256, smem, s>>>((const double*)d_coeffs, n, d_mean, d_evals, d_evecs, P.d_p,
+                                                   P.d_coef_off, P.d_evec_off, sigma2, mode, n_total, (double*)d_out);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace fbspca

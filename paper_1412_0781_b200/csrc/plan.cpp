@@ -1,0 +1,258 @@
+// plan.cpp -- host-side precomputation (Alg. 1 lines 1-2).  Untimed, fp64.
+//
+// Independent of oracle/: Bessel values come from libm jn(), roots by sign scan + bisection +
+// Newton, Gauss-Legendre by Newton on the Legendre recurrence, and the NUFFT window/deapodisation
+// are product-only (the oracle uses a direct Fourier sum).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace fbspca {
+
+namespace {
+
+double bessel_j(int k, double x) { return jn(k, x); }
+
+// All positive zeros of J_k up to xmax, plus the first above (P:87 R_{k,q}).  A sign scan of step
+// 0.25 (< pi, below the spacing of consecutive zeros) brackets each root; J_k has no zero below k.
+std::vector<double> bessel_zeros_upto(int k, double xmax) {
+  std::vector<double> roots;
+  const double step = 0.25;
+  double x = std::max(double(k), 0.05);
+  double fx = bessel_j(k, x);
+  while (true) {
+    double x2 = x + step;
+    double f2 = bessel_j(k, x2);
+    if ((fx < 0 && f2 > 0) || (fx > 0 && f2 < 0)) {
+      double a = x, b = x2, fa = fx;
+      for (int it = 0; it < 200 && b - a > 1e-15 * b; ++it) {     // bisection
+        double m = 0.5 * (a + b), fm = bessel_j(k, m);
+        if ((fa < 0) == (fm < 0)) { a = m; fa = fm; } else { b = m; }
+      }
+      double r = 0.5 * (a + b);
+      for (int it = 0; it < 3; ++it) {                            // Newton polish, J_k' = (J_{k-1}-J_{k+1})/2
+        double d = 0.5 * (bessel_j(k - 1, r) - bessel_j(k + 1, r));
+        if (d == 0) break;
+        double nr = r - bessel_j(k, r) / d;
+        if (!(std::fabs(nr - r) < 0.5)) break;
+        r = nr;
+      }
+      roots.push_back(r);
+      if (r > xmax) break;
+    }
+    x = x2; fx = f2;
+  }
+  return roots;
+}
+
+// n-point Gauss-Legendre on [a,b]: Newton on P_n from cos(pi (i - 1/4)/(n + 1/2)).
+void gauss_legendre(int n, double a, double b, std::vector<double>& x, std::vector<double>& w) {
+  x.assign(n, 0); w.assign(n, 0);
+  for (int i = 0; i < (n + 1) / 2; ++i) {
+    double z = std::cos(M_PI * (i + 0.75) / (n + 0.5)), pp = 0;
+    for (int it = 0; it < 100; ++it) {
+      double p1 = 1, p2 = 0;
+      for (int j = 1; j <= n; ++j) { double p3 = p2; p2 = p1; p1 = ((2 * j - 1) * z * p2 - (j - 1) * p3) / j; }
+      pp = n * (z * p1 - p2) / (z * z - 1);
+      double z1 = z;
+      z = z1 - p1 / pp;
+      if (std::fabs(z - z1) < 1e-16) break;
+    }
+    {   // final derivative at the converged root
+      double p1 = 1, p2 = 0;
+      for (int j = 1; j <= n; ++j) { double p3 = p2; p2 = p1; p1 = ((2 * j - 1) * z * p2 - (j - 1) * p3) / j; }
+      pp = n * (z * p1 - p2) / (z * z - 1);
+    }
+    double wi = 2.0 / ((1 - z * z) * pp * pp);
+    // node -z (ascending order from a), +z mirrored
+    x[i] = a + (b - a) * (1 - z) / 2;       x[n - 1 - i] = a + (b - a) * (1 + z) / 2;
+    w[i] = wi * (b - a) / 2;                w[n - 1 - i] = wi * (b - a) / 2;
+  }
+}
+
+// Exponential-of-semicircle window phi(y) = exp(beta (sqrt(1 - (2y/w)^2) - 1)), |y| <= w/2 (grid units),
+// and its Fourier transform Phi(t) = int phi(y) e^{-2 pi i y t} dy, via y = (w/2) sin u (smooth in u).
+double es_Phi(double t, int w, double beta) {
+  static thread_local std::vector<double> gx, gw;
+  if (gx.empty()) gauss_legendre(256, 0.0, M_PI / 2, gx, gw);
+  double s = 0, hw = 0.5 * w;
+  for (size_t i = 0; i < gx.size(); ++i) {
+    double y = hw * std::sin(gx[i]);
+    s += gw[i] * std::exp(beta * (std::cos(gx[i]) - 1.0)) * std::cos(2 * M_PI * y * t) * hw * std::cos(gx[i]);
+  }
+  return 2 * s;
+}
+
+bool smooth5(int n) { for (int f : {2, 3, 5}) while (n % f == 0) n /= f; return n == 1; }
+
+FftPlan make_fft(int n) {
+  FftPlan f; f.n = n;
+  int m = n;
+  auto push = [&](int r) { f.radix[f.nstages++] = r; m /= r; };
+  while (m % 8 == 0 && f.nstages < kMaxRadixStages) push(8);
+  while (m % 4 == 0 && f.nstages < kMaxRadixStages) push(4);
+  while (m % 2 == 0 && f.nstages < kMaxRadixStages) push(2);
+  while (m % 5 == 0 && f.nstages < kMaxRadixStages) push(5);
+  while (m % 3 == 0 && f.nstages < kMaxRadixStages) push(3);
+  if (m != 1) f.nstages = -1;
+  return f;
+}
+
+int ceil_guard(double x) { return int(std::ceil(x - 1e-9)); }   // reading Q4
+
+}  // namespace
+
+int fft_values_per_lane(const FftPlan& f) {
+  int v = 0;
+  for (int s = 0; s < f.nstages; ++s) {
+    int nb = f.n / f.radix[s];
+    v = std::max(v, ((nb + 31) / 32) * f.radix[s]);
+  }
+  return v;
+}
+
+fbspca_status build_host_plan(Plan& P) {
+  const double c = P.c, R = P.R;
+  const int L = P.L;
+  if (!(c > 0 && c <= 0.5)) { set_error("c must be in (0, 1/2] (P:78)"); return FBSPCA_ERR_CONFIG; }
+  if (L < 4) { set_error("L must be >= 4"); return FBSPCA_ERR_CONFIG; }
+  if (!(R >= 2) || c * R < 1) { set_error("R >= 2 and cR >= 1 required (empty basis otherwise)"); return FBSPCA_ERR_CONFIG; }
+  if (R > 0.5 * L) { set_error("R must be <= L/2"); return FBSPCA_ERR_CONFIG; }
+  if (!(P.eps >= 1e-14 && P.eps <= 1e-3)) { set_error("eps must be in [1e-14, 1e-3]"); return FBSPCA_ERR_CONFIG; }
+  if (P.dt == FBSPCA_F32 && P.eps < 1e-6) { set_error("eps below the fp32 floor 1e-6"); return FBSPCA_ERR_CONFIG; }
+
+  // ---- census (Eq. (criterion1)) ----
+  const double X = 2 * M_PI * c * R;
+  P.p.clear(); P.zeros.clear(); P.norm.clear();
+  for (int k = 0;; ++k) {
+    std::vector<double> z = bessel_zeros_upto(k, X);
+    int pk = 0;
+    for (size_t q = 1; q < z.size(); ++q) if (z[q] <= X) ++pk;
+    if (pk == 0) break;
+    P.p.push_back(pk);
+    for (int q = 0; q < pk; ++q) {
+      P.zeros.push_back(z[q]);
+      P.norm.push_back(1.0 / (c * std::sqrt(M_PI) * std::fabs(bessel_j(k + 1, z[q]))));   // N_{k,q}
+    }
+  }
+  P.k_max = int(P.p.size()) - 1;
+  const int nk = P.k_max + 1;
+  P.coef_off.assign(nk + 1, 0); P.blk_off.assign(nk + 1, 0); P.evec_off.assign(nk + 1, 0);
+  for (int k = 0; k < nk; ++k) {
+    P.coef_off[k + 1] = P.coef_off[k] + P.p[k];
+    P.blk_off[k + 1] = P.blk_off[k] + int64_t(P.p[k]) * (P.p[k] + 1) / 2;
+    P.evec_off[k + 1] = P.evec_off[k] + int64_t(P.p[k]) * P.p[k];
+  }
+
+  // ---- quadrature grid and radial table ----
+  P.n_xi = ceil_guard(4 * c * R);
+  P.n_theta = ceil_guard(16 * c * R);
+  if (P.n_theta % 2) { set_error("n_theta = ceil(16cR) must be even (half-plane symmetry)"); return FBSPCA_ERR_CONFIG; }
+  if (2 * P.k_max >= P.n_theta) { set_error("k_max >= n_theta/2"); return FBSPCA_ERR_CONFIG; }
+  gauss_legendre(P.n_xi, 0.0, c, P.xi, P.wq);
+  const int64_t ncoef = P.coef_off[nk];
+  P.table.assign(size_t(ncoef) * P.n_xi, 0.0);
+  const double ang = 2 * M_PI / P.n_theta;        // Eq. (1DFFT) weight, folded into the table
+  for (int k = 0; k < nk; ++k)
+    for (int q = 0; q < P.p[k]; ++q) {
+      int64_t row = P.coef_off[k] + q;
+      double Rq = P.zeros[row], N = P.norm[row];
+      for (int j = 0; j < P.n_xi; ++j)
+        P.table[row * P.n_xi + j] = N * bessel_j(k, Rq * P.xi[j] / c) * P.xi[j] * P.wq[j] * ang;
+    }
+
+  // ---- NUFFT: oversampled grid, window, deapodisation ----
+  int M = 2 * L;
+  while (!smooth5(M) || M % 2) ++M;
+  P.M = M;
+  int w = int(std::ceil(-std::log10(P.eps) - 1e-9)) + 1;         // error ~ 10^{-(w-1)} at sigma = 2
+  if (P.dt == FBSPCA_F32) { w = std::max(6, std::min(w, 8)); }
+  else { w = std::max(w, 13); if (w > 13) w = 13; }
+  P.w = w;
+  P.beta = 2.30 * w;
+  if (P.dt == FBSPCA_F32) P.beta = double(float(P.beta));   // the fp32 kernel evaluates phi with a float beta
+  P.deapod.assign(L, 0.0);
+  for (int a = 0; a < L; ++a) {
+    int i = a - L / 2;
+    P.deapod[a] = 1.0 / es_Phi(double(i) / M, w, P.beta);
+  }
+
+  // ---- polar nodes (half plane, theta in [0, pi)), column phases ----
+  const int half = P.n_theta / 2;
+  const double hw = 0.5 * w;
+  std::vector<double> rho(P.n_xi), cs(2 * half);
+  for (int j = 0; j < P.n_xi; ++j) rho[j] = P.xi[j] * M;
+  for (int l = 0; l < half; ++l) {
+    double th = 2 * M_PI * l / P.n_theta;
+    cs[2 * l] = std::cos(th); cs[2 * l + 1] = std::sin(th);
+  }
+  std::vector<int> b2(size_t(P.n_xi) * half);
+  int b2min = 1 << 30, b2max = -(1 << 30);
+  for (int j = 0; j < P.n_xi; ++j)
+    for (int l = 0; l < half; ++l) {
+      double k2 = rho[j] * cs[2 * l + 1];
+      int b = int(std::ceil(k2 - hw));
+      b2[size_t(j) * half + l] = b;
+      b2min = std::min(b2min, b); b2max = std::max(b2max, b);
+    }
+  PolarParams& pp = P.pp;
+  pp = PolarParams{};
+  pp.L = L; pp.M = M; pp.w = w; pp.n_xi = P.n_xi; pp.n_theta = P.n_theta; pp.half = half; pp.k_max = P.k_max;
+  pp.col_lo = b2min; pp.ncols_x = b2max + w - b2min;
+  pp.beta = P.beta; pp.half_w = hw;
+  pp.fft_M = make_fft(M); pp.fft_theta = make_fft(P.n_theta);
+  if (pp.fft_M.nstages < 0 || pp.fft_theta.nstages < 0) { set_error("FFT sizes must be 2^a 3^b 5^c"); return FBSPCA_ERR_CONFIG; }
+  pp.nwarps = 16;
+  const int csz = (P.dt == FBSPCA_F32) ? 8 : 16;       // sizeof complex
+  const int fixed = polar_fixed_smem(M, P.n_theta, L, csz, pp.nwarps);
+  const int budget = polar_max_smem() - fixed;
+  const int kk = (P.k_max + 1) | 1;                    // staging row stride (odd)
+  const int ang_scr = pp.nwarps * 2 * P.n_theta * csz;
+  if (budget < ang_scr + kk * csz || budget < M * 11 * csz) {
+    set_error("image too large for the fused polar kernel's shared memory"); return FBSPCA_ERR_CONFIG;
+  }
+  int S = budget / (M * csz);
+  if (S % 2 == 0) --S;                                   // odd row stride (bank spread)
+  if (S > pp.ncols_x) S = pp.ncols_x | 1;
+  pp.S = S;
+  int G = (budget - ang_scr) / (kk * csz);
+  G = std::max(1, std::min(G, std::min(32, P.n_xi)));
+  pp.ring_group = G;
+  const int region = std::max(M * S * csz, ang_scr + G * kk * csz);
+  pp.smem_region_bytes = region;
+  P.polar_smem = fixed + region;
+  // phases over columns: phase p holds m2 in [lo_p, lo_p + S) and owns nodes with b2 in [lo_p, lo_p + S - w]
+  std::vector<int> order(b2.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return b2[a] < b2[b]; });
+  P.nodes.clear();
+  int np = 0, lo = b2min;
+  size_t pos = 0;
+  while (pos < order.size()) {
+    if (np >= kMaxPhases) { set_error("too many column phases"); return FBSPCA_ERR_CONFIG; }
+    pp.phase_lo[np] = lo;
+    pp.phase_node_begin[np] = int(P.nodes.size());
+    std::vector<uint32_t> ph;
+    while (pos < order.size() && b2[order[pos]] <= lo + S - w) {
+      int id = order[pos++];
+      int j = id / half, l = id % half;
+      ph.push_back((uint32_t(j) << 16) | uint32_t(l));
+    }
+    std::sort(ph.begin(), ph.end());                      // ring-major within a phase
+    P.nodes.insert(P.nodes.end(), ph.begin(), ph.end());
+    ++np;
+    lo = lo + S - w + 1;
+  }
+  pp.n_phase = np;
+  pp.phase_node_begin[np] = int(P.nodes.size());
+  P.rho = rho;
+  P.cs = cs;
+  return FBSPCA_OK;
+}
+
+}  // namespace fbspca

@@ -1,0 +1,104 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol include/fbspca.h declares, and its
+host-side plan (census, GL rule, radial table, errors) agrees with the oracle.  No compute calls."""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+from scipy.special import jv
+
+import oracle as O
+import paper_1412_0781_b200 as F
+from paper_1412_0781_b200._lib import LIB_PATH, SIGNATURES, FbspcaError, lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    import __graft_entry__ as g
+    g.build()
+
+
+def test_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "fbspca.h")).read()
+    declared = set(re.findall(r"\b(fbspca_[a-z_]+)\s*\(", hdr))
+    declared = {d for d in declared if d not in ("fbspca_plan_t", "fbspca_stream_t")}
+    assert declared, "no declarations parsed"
+    L = lib()
+    for name in sorted(declared):
+        assert hasattr(L, name), f"{name} declared in fbspca.h but not exported by {LIB_PATH}"
+    assert declared == set(SIGNATURES), "binding signatures out of sync with the header"
+    assert b"sm_100a" in L.fbspca_version()
+
+
+@pytest.mark.parametrize("L,R", [(32, 16), (33, 16), (64, 32), (128, 64)])
+def test_host_plan_matches_oracle(L, R):
+    pl = F.fbspca_plan(L, 0.5, R, device=-1)
+    b = O.build_basis(0.5, R)
+    assert pl.k_max == b.k_max and np.array_equal(pl.p, b.p)
+    assert pl.n_xi == b.n_xi and pl.n_theta == b.n_theta
+    zo = np.concatenate([z[:pk] for z, pk in zip(b.zeros, b.p)])
+    assert np.max(np.abs(pl.zeros - zo)) < 1e-11
+    xo, wo, _ = O.polar_grid(b)
+    assert np.max(np.abs(pl.xi - xo)) < 1e-15 and np.max(np.abs(pl.wq - wo) / wo) < 1e-10
+    assert np.array_equal(pl.coef_off, b.coef_off)
+    assert pl.blk_off[-1] == sum(pk * (pk + 1) // 2 for pk in b.p)
+    assert pl.n_theta % 2 == 0 and pl.M >= 2 * L
+
+
+def test_plan_window_and_phases():
+    pl = F.fbspca_plan(128, 0.5, 64, device=-1)
+    assert pl.w == 6 and abs(pl.beta - 2.3 * 6) < 1e-12 and pl.M == 256
+    assert 1 <= pl.n_phase <= 4 and pl.smem_bytes <= 227 * 1024
+    pl64 = F.fbspca_plan(32, 0.5, 16, dtype=F.F64, device=-1)
+    assert pl64.w == 13
+
+
+@pytest.mark.parametrize("args,code", [
+    ((64, 0.6, 32), "CONFIG"), ((64, 0.5, 40), "CONFIG"), ((64, 0.5, 1.5), "CONFIG"),
+    ((64, 0.05, 10), "CONFIG"), ((2, 0.5, 1), "CONFIG"),
+])
+def test_plan_config_errors(args, code):
+    with pytest.raises(FbspcaError, match=code):
+        F.fbspca_plan(*args, device=-1)
+
+
+def test_plan_eps_errors():
+    with pytest.raises(FbspcaError, match="CONFIG"):
+        F.fbspca_plan(64, 0.5, 32, eps=1e-8, device=-1)           # below the fp32 floor
+    with pytest.raises(FbspcaError, match="CONFIG"):
+        F.fbspca_plan(64, 0.5, 32, eps=1e-2, device=-1)
+    F.fbspca_plan(64, 0.5, 32, eps=1e-8, dtype=F.F64, device=-1)
+
+
+def test_host_only_plan_refuses_compute():
+    import ctypes
+    pl = F.fbspca_plan(32, 0.5, 16, device=-1)
+    st = lib().fbspca_expand(ctypes.c_void_p(pl.handle), ctypes.c_void_p(16), 1, ctypes.c_void_p(16), None)
+    assert st == 1 and b"host-only" in lib().fbspca_last_error()
+
+
+def test_shard_range_partitions():
+    for n in (1, 7, 100, 100_000):
+        for world in (1, 2, 3, 8):
+            spans = [F.shard_range(n, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            sizes = [e - s for s, e in spans]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_unpack_blocks_layout():
+    pl = F.fbspca_plan(32, 0.5, 16, device=-1)
+    rng = np.random.default_rng(0)
+    mats = []
+    packed = np.zeros(pl.n_blk)
+    for k in range(pl.k_max + 1):
+        pk = int(pl.p[k])
+        A = rng.standard_normal((pk, pk)); A = A + A.T
+        mats.append(A)
+        packed[pl.blk_off[k]:pl.blk_off[k + 1]] = A[np.triu_indices(pk)]
+    got = F.unpack_blocks(pl, packed)
+    assert all(np.array_equal(a, b) for a, b in zip(got, mats))

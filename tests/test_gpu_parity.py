@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): per-image coefficient relative l2 <= 1e-4 (reading Q12: k > 0 counted twice),
+top-50 eigenvalues within 1e-4 relative, principal-subspace cosine >= 0.9999.  fp64 (C1) is held to 1e-9.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_1412_0781_b200 as F
+import synth
+
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda:0") if torch.cuda.is_available() else None
+TOL32 = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as g
+    g.build()
+
+
+def rel_l2_per_image(got, ref, basis):
+    """Reading Q12: || a_gpu - a_orc || / || a_orc || per image, k > 0 rows weighted x2 (the +-k norm)."""
+    wt = np.ones(ref.shape[0])
+    wt[basis.p[0]:] = 2.0
+    num = np.sqrt((wt[:, None] * np.abs(got - ref) ** 2).sum(0))
+    den = np.sqrt((wt[:, None] * np.abs(ref) ** 2).sum(0))
+    return num / den
+
+
+def gpu_expand(plan, imgs_t):
+    c = F.fbspca_expand(plan, imgs_t)
+    torch.cuda.synchronize()
+    return c.cpu().numpy().astype(np.complex128)
+
+
+def blob_case(name, first, n, **kw):
+    cfg = synth.config(name)
+    imgs = synth.blob_images(cfg, first, n, device=DEV)
+    return cfg, imgs
+
+
+# ------------------------------------------------------------------ expansion (Alg. 1)
+@pytest.mark.parametrize("name,n,max_batch", [("C2", 40, 4096), ("C2", 37, 16), ("C3", 12, 5)])
+def test_expand_parity_blobs(name, n, max_batch):
+    cfg, imgs = blob_case(name, 0, n)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=max_batch)
+    got = gpu_expand(plan, imgs)
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    ref = O.to_flat(O.expand(imgs.double().cpu().numpy(), basis))
+    rel = rel_l2_per_image(got, ref, basis)
+    assert rel.max() <= TOL32, f"max per-image rel l2 {rel.max():.3e}"
+    assert np.all(got[: basis.p[0]].imag == 0)                    # Q8
+
+
+def test_expand_parity_c1_fp64():
+    imgs = synth.c1_images(256)
+    plan = F.fbspca_plan(32, 0.5, 16, dtype=F.F64, device=0)
+    got = gpu_expand(plan, torch.from_numpy(imgs).to(DEV))
+    basis = O.build_basis(0.5, 16)
+    ref = O.to_flat(O.expand(imgs, basis))
+    rel = rel_l2_per_image(got, ref, basis)
+    print("C1 fp64 max per-image rel l2", rel.max())
+    assert rel.max() <= 1e-9
+
+
+@pytest.mark.parametrize("L,R", [(33, 16), (20, 10)])
+def test_expand_odd_and_small_L(L, R):
+    rng = np.random.default_rng(L)
+    imgs = rng.standard_normal((5, L, L)).astype(np.float32)
+    plan = F.fbspca_plan(L, 0.5, R, device=0)
+    got = gpu_expand(plan, torch.from_numpy(imgs).to(DEV))
+    basis = O.build_basis(0.5, R)
+    ref = O.to_flat(O.expand(imgs.astype(np.float64), basis))
+    assert rel_l2_per_image(got, ref, basis).max() <= TOL32
+
+
+def test_expand_single_image_and_errors():
+    cfg, imgs = blob_case("C2", 7, 1)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0)
+    got = gpu_expand(plan, imgs)
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    ref = O.to_flat(O.expand(imgs.double().cpu().numpy(), basis))
+    assert rel_l2_per_image(got, ref, basis).max() <= TOL32
+    with pytest.raises(F.FbspcaError, match="ARG"):
+        F.fbspca_expand(plan, imgs[:0])
+
+
+def test_expand_rotation_reflection_on_gpu():
+    """Eq. (rot)/(refl): rot90 -> a e^{-ik pi/2}, flip axis 0 -> conj(a), on the CUDA path (odd L)."""
+    rng = np.random.default_rng(9)
+    I = rng.standard_normal((1, 33, 33)).astype(np.float32)
+    batch = np.concatenate([I, np.rot90(I, 1, axes=(1, 2)), I[:, ::-1, :]]).copy()
+    plan = F.fbspca_plan(33, 0.5, 16, device=0)
+    a = gpu_expand(plan, torch.from_numpy(batch).to(DEV))
+    basis = O.build_basis(0.5, 16)
+    A = O.from_flat(a, basis)
+    scale = np.abs(a[:, 0]).max()
+    for k in range(basis.k_max + 1):
+        assert np.max(np.abs(A[k][:, 1] - A[k][:, 0] * np.exp(-1j * k * np.pi / 2))) <= 1e-4 * scale
+        assert np.max(np.abs(A[k][:, 2] - np.conj(A[k][:, 0]))) <= 1e-4 * scale
+
+
+@pytest.mark.parametrize("name,n", [("C4", 2), ("C5", 1)])
+def test_expand_parity_large_L(name, n):
+    cfg, imgs = blob_case(name, 0, n)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=64)
+    got = gpu_expand(plan, imgs)
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    ref = O.to_flat(O.expand(imgs.double().cpu().numpy(), basis, chunk=1))
+    rel = rel_l2_per_image(got, ref, basis)
+    assert rel.max() <= TOL32, f"{name}: {rel.max():.3e}"
+
+
+# ------------------------------------------------------------------ covariance / eig / projection (Alg. 2)
+def _subspace_cos(Ug, Uo, lam_o, r):
+    """sigma_min(U_gpu[:, :r]^T U_orc[:, :r]), r extended across near-ties (Q10)."""
+    while r < len(lam_o) and abs(lam_o[r - 1] - lam_o[r]) <= 1e-3 * abs(lam_o[r - 1]):
+        r += 1
+    s = np.linalg.svd(Ug[:, :r].T @ Uo[:, :r], compute_uv=False)
+    return s.min()
+
+
+def test_spca_parity_c2_subset():
+    cfg, imgs = blob_case("C2", 0, 600)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=256)
+    coeffs = F.fbspca_expand(plan, imgs)
+    blocks, mean = F.fbspca_covariance(plan, coeffs)
+    evals, evecs = F.fbspca_eig(plan, blocks)
+    sigma2 = (synth.blobs.noise_sigma(cfg, device=DEV)) ** 2
+    out = F.fbspca_project(plan, coeffs, mean, evals, evecs, sigma2=sigma2, mode=1)
+    torch.cuda.synchronize()
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    A = O.expand(imgs.double().cpu().numpy(), basis)
+    m_o, C_o = O.block_covariance(A)
+    lam_o, U_o = O.block_eig(C_o)
+    # covariance blocks
+    C_g = F.unpack_blocks(plan, blocks.cpu().numpy())
+    scale = max(np.abs(c).max() for c in C_o)
+    assert max(np.abs(a - b).max() for a, b in zip(C_g, C_o)) <= 1e-4 * scale
+    assert np.allclose(mean.cpu().numpy(), m_o, atol=1e-4 * np.abs(m_o).max())
+    # top-50 eigenvalues (Q11 pooling)
+    lam_g, U_g = F.split_eig(plan, evals.cpu().numpy(), evecs.cpu().numpy())
+    pool_o = sorted(((-l, k, i) for k, lk in enumerate(lam_o) for i, l in enumerate(lk)))[:50]
+    worst = max(abs(lam_g[k][i] - lam_o[k][i]) / abs(lam_o[k][i]) for _, k, i in pool_o)
+    assert worst <= 1e-4, f"top-50 eigenvalue rel err {worst:.2e}"
+    # principal subspaces per k
+    for k in sorted({k for _, k, _ in pool_o}):
+        r = sum(1 for _, kk, _ in pool_o if kk == k)
+        assert _subspace_cos(U_g[k], U_o[k], lam_o[k], r) >= 0.9999
+    # eigvec orthonormality on the GPU
+    for Uk in U_g:
+        assert np.allclose(Uk.T @ Uk, np.eye(Uk.shape[0]), atol=1e-10)
+    # projection + MP/Wiener filter (mode 1) on well-separated leading components
+    ref = O.project(A, m_o, U_o, lam_o, basis, sigma2, 1, A[0].shape[1])
+    got = O.from_flat(out.cpu().numpy().astype(np.complex128), basis)
+    for k in range(basis.k_max + 1):
+        gaps = np.abs(np.diff(lam_o[k])) / np.maximum(np.abs(lam_o[k][:-1]), 1e-30)
+        for l in range(min(3, basis.p[k])):
+            if l < len(gaps) and gaps[l] > 1e-2 and (l == 0 or gaps[l - 1] > 1e-2):
+                nrm = np.linalg.norm(ref[k][l]) + 1e-30
+                assert np.linalg.norm(got[k][l] - ref[k][l]) <= 1e-3 * nrm + 1e-6 * np.linalg.norm(A[k])
+
+
+def test_spca_parity_c1_fp64():
+    imgs = synth.c1_images(256)
+    plan = F.fbspca_plan(32, 0.5, 16, dtype=F.F64, device=0)
+    coeffs = F.fbspca_expand(plan, torch.from_numpy(imgs).to(DEV))
+    blocks, mean = F.fbspca_covariance(plan, coeffs)
+    evals, evecs = F.fbspca_eig(plan, blocks)
+    out = F.fbspca_project(plan, coeffs, mean, evals, evecs)
+    torch.cuda.synchronize()
+    basis = O.build_basis(0.5, 16)
+    A = O.expand(imgs, basis)
+    m_o, C_o = O.block_covariance(A)
+    lam_o, U_o = O.block_eig(C_o)
+    C_g = F.unpack_blocks(plan, blocks.cpu().numpy())
+    scale = max(np.abs(c).max() for c in C_o)
+    assert max(np.abs(a - b).max() for a, b in zip(C_g, C_o)) <= 1e-9 * scale
+    lam_g, U_g = F.split_eig(plan, evals.cpu().numpy(), evecs.cpu().numpy())
+    for lg, lo in zip(lam_g, lam_o):
+        assert np.max(np.abs(lg - lo)) <= 1e-9 * max(1.0, np.abs(lo).max())
+    got = O.from_flat(out.cpu().numpy(), basis)
+    _, Ac = O.mean_and_center(A)
+    for gk, ak in zip(got, Ac):      # orthonormal change of basis preserves per-image norms
+        assert np.allclose(np.linalg.norm(gk, axis=0), np.linalg.norm(ak, axis=0), rtol=1e-8, atol=1e-12)
+
+
+def test_eig_random_spd_blocks_vs_numpy():
+    """K6 alone: feed packed random symmetric blocks (p up to 63) and compare with eigh."""
+    plan = F.fbspca_plan(128, 0.5, 64, device=0)
+    rng = np.random.default_rng(11)
+    packed = np.zeros(plan.n_blk)
+    mats = []
+    for k in range(plan.k_max + 1):
+        pk = int(plan.p[k])
+        X = rng.standard_normal((pk, pk + 3))
+        Cm = X @ X.T / (pk + 3) + np.diag(np.linspace(0, 1, pk))
+        mats.append(Cm)
+        packed[plan.blk_off[k]:plan.blk_off[k + 1]] = Cm[np.triu_indices(pk)]
+    evals, evecs = F.fbspca_eig(plan, torch.from_numpy(packed).to(DEV))
+    lam_g, U_g = F.split_eig(plan, evals.cpu().numpy(), evecs.cpu().numpy())
+    lam_o, U_o = O.block_eig(mats)
+    for Cm, lg, lo, Ug in zip(mats, lam_g, lam_o, U_g):
+        assert np.max(np.abs(lg - lo)) <= 1e-11 * np.abs(lo).max()
+        assert np.allclose(Ug @ np.diag(lg) @ Ug.T, Cm, atol=1e-11 * np.abs(Cm).max())
+
+
+def test_covariance_virtual_shards_and_partial_api():
+    """Sum of shard partials (shards aligned to the 4096-image accumulation batches) == the full partial."""
+    cfg, imgs = blob_case("C2", 0, 10_000)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0)
+    coeffs = F.fbspca_expand(plan, imgs)
+    full = F.fbspca_covariance_partial(plan, coeffs).clone()
+    parts = []
+    for s, e in ((0, 4096), (4096, 8192), (8192, 10_000)):
+        parts.append(F.fbspca_covariance_partial(plan, coeffs[:, s:e].contiguous()).clone())
+    tot = sum(parts)
+    assert torch.allclose(tot, full, rtol=1e-12, atol=1e-9)
+    b1, m1 = F.fbspca_covariance_finalize(plan, tot)
+    b2, m2 = F.fbspca_covariance(plan, coeffs)
+    assert torch.allclose(b1, b2, rtol=1e-12, atol=1e-12) and torch.allclose(m1, m2)
+    # PSD + symmetry of the finalised blocks
+    for Ck in F.unpack_blocks(plan, b2.cpu().numpy()):
+        assert np.linalg.eigvalsh(Ck).min() >= -1e-6 * np.abs(Ck).max()
+
+
+def test_c3_full_size_sampled_parity():
+    """BASELINE configs[2] at full size in bench's launch configuration; sampled images vs the oracle."""
+    cfg = synth.config("C3")
+    n = cfg["n"]
+    imgs = synth.blob_images(cfg, 0, n, device=DEV)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0)
+    coeffs = F.fbspca_expand(plan, imgs)
+    blocks, mean = F.fbspca_covariance(plan, coeffs)
+    torch.cuda.synchronize()
+    idx = [0, 1, 4095, 4096, 55_555, n - 1]
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    ref = O.to_flat(O.expand(imgs[idx].double().cpu().numpy(), basis))
+    got = coeffs[:, idx].cpu().numpy().astype(np.complex128)
+    assert rel_l2_per_image(got, ref, basis).max() <= TOL32
+    # properties at full size: mean and trace bookkeeping from the GPU coefficients
+    A0 = coeffs[: plan.p[0]].real.double()
+    assert torch.allclose(mean, A0.mean(1), rtol=1e-6, atol=1e-7)
+    tr = F.unpack_blocks(plan, blocks.cpu().numpy())
+    k = 5
+    Ak = coeffs[plan.coef_off[k]:plan.coef_off[k + 1]]
+    assert abs(np.trace(tr[k]) - (Ak.abs() ** 2).double().sum().item() / n) <= 1e-5 * np.trace(tr[k])
