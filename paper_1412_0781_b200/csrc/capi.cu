@@ -150,6 +150,7 @@ fbspca_status upload_plan(Plan& P) {
   FB_CUDA(cudaMalloc(&P.d_ghat, (size_t)nk * P.max_batch * 2 * P.n_xi * rsz), "alloc ghat");
   const int64_t npart = P.blk_off[nk] + P.p[0] + 1;
   FB_CUDA(cudaMalloc((void**)&P.d_partial, npart * sizeof(double)), "alloc partial");
+  FB_CUDA(cudaMalloc((void**)&P.d_cov_scratch, (size_t)kCovMaxChunks * npart * sizeof(double)), "alloc cov scratch");
   FB_CUDA(upload((void**)&P.d_p, P.p.data(), P.p.size()), "upload p");
   FB_CUDA(upload((void**)&P.d_coef_off, P.coef_off.data(), P.coef_off.size()), "upload coef_off");
   FB_CUDA(upload((void**)&P.d_blk_off, P.blk_off.data(), P.blk_off.size()), "upload blk_off");
@@ -169,7 +170,7 @@ void free_plan(Plan& P) {
   DeviceGuard g(P.device);
   void* ptrs[] = {P.d_table, P.d_deapod, P.d_tw_M, P.d_tw_theta, P.d_rho, P.d_cs, P.d_nodes, P.d_xscratch,
                   P.d_pscratch, P.d_ghat, P.d_partial, P.d_p, P.d_coef_off, P.d_blk_off, P.d_evec_off,
-                  P.d_eig_work, P.d_eig_sweeps, P.d_coef_k, P.d_pp};
+                  P.d_eig_work, P.d_eig_sweeps, P.d_coef_k, P.d_pp, P.d_cov_scratch};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& ev : P.tevents) { cudaEventDestroy(ev.second.first); cudaEventDestroy(ev.second.second); }
 }
@@ -274,7 +275,7 @@ static fbspca_status cov_accumulate(fbspca_plan_t h, const void* d_coeffs, int64
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t npart = P.blk_off[P.k_max + 1] + P.p[0] + 1;
   if (zero) FB_CUDA(cudaMemsetAsync(d_partial, 0, npart * sizeof(double), s), "memset partial");
-  const int64_t B = 4096;
+  const int64_t B = kCovBatch;
   TimedRegion t(P, T_COV, s);
   for (int64_t i0 = 0; i0 < n_local; i0 += B) {
     const int64_t nb = std::min<int64_t>(B, n_local - i0);

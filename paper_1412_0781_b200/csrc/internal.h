@@ -13,6 +13,9 @@ namespace fbspca {
 
 constexpr int kMaxRadixStages = 16;
 constexpr int kMaxPhases = 64;
+constexpr int kCovChunk = 512;          // images per covariance split-K chunk
+constexpr int kCovBatch = 16384;        // images per covariance launch
+constexpr int kCovMaxChunks = kCovBatch / kCovChunk;
 
 // Stockham radix plan for a length-N FFT (N = prod radices; radices in {2,3,4,5,8}).
 struct FftPlan {
@@ -31,7 +34,9 @@ struct PolarParams {
   int phase_node_begin[kMaxPhases + 1];
   double beta;
   double half_w;                  // w/2
-  int nwarps;
+  int nwarps;                     // warps per CTA (gather, fills)
+  int fft_warps;                  // warps owning row/column FFT scratch
+  int ang_warps;                  // warps running ring FFTs
   int ring_group;                 // rings staged together in the angular pass
   int smem_region_bytes;          // bytes of the shared work region (complex units * sizeof)
   FftPlan fft_M, fft_theta;
@@ -88,6 +93,7 @@ struct Plan {
   void* d_pscratch = nullptr;
   void* d_ghat = nullptr;                // (k_max+1) x max_batch x 2 x n_xi  (T)
   double* d_partial = nullptr;           // blk_off[k_max+1] + p_0 + 1
+  double* d_cov_scratch = nullptr;       // kCovMaxChunks x (blk_off[k_max+1] + p_0 + 1)
   int* d_coef_k = nullptr;               // row -> k lookup (coef rows)
   int* d_p = nullptr;
   int64_t* d_coef_off = nullptr;

@@ -125,15 +125,17 @@ __device__ void cov_tile(const T* __restrict__ Ak, int pk, int64_t ld2, int64_t 
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int q = qa + tx + 16 * i, qq = qb + ty + 16 * j;
-      if (q < pk && qq < pk && q <= qq) dst[packed_idx(q, qq, pk)] += double(acc[i][j]);
+      if (q < pk && qq < pk && q <= qq) dst[packed_idx(q, qq, pk)] = double(acc[i][j]);
     }
 }
 
+// Split-K: CTA (k, tile pair, chunk) sums its kCovChunk images of the batch and STORES the chunk's partial
+// (fp64) into scratch[chunk][.]; cov_reduce_kernel then adds the chunks in fixed order -> deterministic.
 template <typename T>
 __global__ void __launch_bounds__(256)
 cov_accum_kernel(const T* __restrict__ coeffs, const int* __restrict__ p, const int64_t* __restrict__ coef_off,
                  const int64_t* __restrict__ blk_off, int64_t ld, int64_t i0, int64_t nb, int k_max,
-                 double* __restrict__ partial) {
+                 double* __restrict__ scratch, int64_t scratch_stride) {
   __shared__ T S1[32][64 + 1];
   __shared__ T S2[32][64 + 1];
   const int k = blockIdx.x;
@@ -143,34 +145,52 @@ cov_accum_kernel(const T* __restrict__ coeffs, const int* __restrict__ p, const 
   while (tq < nt && pair >= nt - tq) { pair -= nt - tq; ++tq; }
   if (tq >= nt) return;
   const int tqq = tq + pair;
+  const int64_t c_img0 = i0 + (int64_t)blockIdx.z * kCovChunk;
+  const int64_t c_nb = min((int64_t)kCovChunk, i0 + nb - c_img0);
   const T* Ak = coeffs + coef_off[k] * 2 * ld;
-  double* dst = partial + blk_off[k];
+  double* dst = scratch + (int64_t)blockIdx.z * scratch_stride + blk_off[k];
   if (k == 0)
-    cov_tile<T, double>(Ak, pk, 2 * ld, 2 * i0, 2 * nb, tq, tqq, dst, S1, S2);
+    cov_tile<T, double>(Ak, pk, 2 * ld, 2 * c_img0, 2 * c_nb, tq, tqq, dst, S1, S2);
   else
-    cov_tile<T, T>(Ak, pk, 2 * ld, 2 * i0, 2 * nb, tq, tqq, dst, S1, S2);
+    cov_tile<T, T>(Ak, pk, 2 * ld, 2 * c_img0, 2 * c_nb, tq, tqq, dst, S1, S2);
   if (k == 0 && blockIdx.y == 0) {
-    double* s0 = partial + blk_off[k_max + 1];
+    double* s0 = scratch + (int64_t)blockIdx.z * scratch_stride + blk_off[k_max + 1];
     for (int q = threadIdx.x; q < pk; q += blockDim.x) {
       double s = 0;
-      const T* row = Ak + (int64_t)q * 2 * ld + 2 * i0;
-      for (int64_t c = 0; c < nb; ++c) s += double(row[2 * c]);
-      s0[q] += s;
+      const T* row = Ak + (int64_t)q * 2 * ld + 2 * c_img0;
+      for (int64_t c = 0; c < c_nb; ++c) s += double(row[2 * c]);
+      s0[q] = s;
     }
-    if (threadIdx.x == 0) s0[pk] += double(nb);
+    if (threadIdx.x == 0) s0[pk] = double(c_nb);
+  }
+}
+
+__global__ void cov_reduce_kernel(const double* __restrict__ scratch, int64_t stride, int nchunk, int64_t total,
+                                  double* __restrict__ partial) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = partial[i];
+    for (int c = 0; c < nchunk; ++c) s += scratch[(int64_t)c * stride + i];
+    partial[i] = s;
   }
 }
 
 cudaError_t launch_cov_accum(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb,
                              double* d_partial, cudaStream_t s) {
   const int nt = (P.p[0] + 63) / 64;
-  dim3 grid((unsigned)(P.k_max + 1), (unsigned)(nt * (nt + 1) / 2));
+  const int nchunk = (int)((nb + kCovChunk - 1) / kCovChunk);
+  if (nchunk > kCovMaxChunks) return cudaErrorInvalidValue;
+  const int64_t total = P.blk_off[P.k_max + 1] + P.p[0] + 1;
+  dim3 grid((unsigned)(P.k_max + 1), (unsigned)(nt * (nt + 1) / 2), (unsigned)nchunk);
   if (P.dt == FBSPCA_F32)
     cov_accum_kernel<float><<<grid, 256, 0, s>>>((const float*)d_coeffs, P.d_p, P.d_coef_off, P.d_blk_off, ld, i0, nb,
-                                                 P.k_max, d_partial);
+                                                 P.k_max, P.d_cov_scratch, total);
   else
     cov_accum_kernel<double><<<grid, 256, 0, s>>>((const double*)d_coeffs, P.d_p, P.d_coef_off, P.d_blk_off, ld, i0,
-                                                  nb, P.k_max, d_partial);
+                                                  nb, P.k_max, P.d_cov_scratch, total);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4 * 148);
+  cov_reduce_kernel<<<blocks, 256, 0, s>>>(P.d_cov_scratch, total, nchunk, total, d_partial);
   return cudaGetLastError();
 }
 

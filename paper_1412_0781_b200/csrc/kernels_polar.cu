@@ -89,86 +89,147 @@ template <typename T2> struct Dft<T2, 5> {
   }
 };
 
-// One out-of-place Stockham stage of radix R (src -> dst, strided), executed by one warp, one
-// butterfly per lane at a time (registers: R complex values).
-template <typename T2, int R>
-__device__ __forceinline__ void fft_stage(const T2* src, int sst, T2* dst, int dstr, int N, int Ns,
-                                          const T2* __restrict__ tw, int lane) {
-  const int NB = N / R;
-  const int step = N / (Ns * R);
-  for (int j = lane; j < NB; j += 32) {
-    T2 v[R];
+// ---------------------------------------------------------------- warp FFTs with load/store functors
+// Stockham (autosort) stage of radix R: butterfly j reads ld(j + r NB), twiddles by w^(r (j mod Ns)),
+// DFT_R, writes st((j / Ns) Ns R + (j mod Ns) + r Ns).  Out of place; one warp; R values in registers.
+template <typename T2, int N, int R, int Ns, class Ld, class St>
+__device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tw, int lane) {
+  constexpr int NB = N / R, step = N / (Ns * R);
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = src[(j + r * NB) * sst];
-    const int jm = j % Ns;
-    const int base = jm * step;
+  for (int j0 = 0; j0 < NB; j0 += 32) {
+    const int j = j0 + lane;
+    if (NB % 32 == 0 || j < NB) {
+      T2 v[R];
 #pragma unroll
-    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[base * r]);
-    Dft<T2, R>::run(v);
-    const int idxD = (j / Ns) * Ns * R + jm;
+      for (int r = 0; r < R; ++r) v[r] = ld(j + r * NB);
+      const int jm = j & (Ns - 1);
+      if constexpr (Ns > 1) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) dst[(idxD + r * Ns) * dstr] = v[r];
+        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[jm * step * r]);
+      }
+      Dft<T2, R>::run(v);
+      const int idxD = (j - jm) * R + jm;
+#pragma unroll
+      for (int r = 0; r < R; ++r) st(idxD + r * Ns, v[r]);
+    }
   }
   __syncwarp();
 }
 
-template <typename T2>
-__device__ __forceinline__ void fft_stage_any(int R, const T2* src, int sst, T2* dst, int dstr, int N, int Ns,
-                                              const T2* tw, int lane) {
+// Compile-time power-of-two FFT: first stage reads ld(), last stage writes st(), ping-pong in A, B.
+template <typename T2, int N, class Ld, class St>
+__device__ __forceinline__ void fft_pow2(Ld ld, St st, T2* A, T2* B, const T2* tw, int lane) {
+  auto lA = [A](int i) { return A[i]; };
+  auto lB = [B](int i) { return B[i]; };
+  auto sA = [A](int i, T2 v) { A[i] = v; };
+  auto sB = [B](int i, T2 v) { B[i] = v; };
+  if constexpr (N == 64) {
+    cstage<T2, 64, 8, 1>(ld, sA, tw, lane); cstage<T2, 64, 8, 8>(lA, st, tw, lane);
+  } else if constexpr (N == 128) {
+    cstage<T2, 128, 8, 1>(ld, sA, tw, lane); cstage<T2, 128, 4, 8>(lA, sB, tw, lane);
+    cstage<T2, 128, 4, 32>(lB, st, tw, lane);
+  } else if constexpr (N == 256) {
+    cstage<T2, 256, 8, 1>(ld, sA, tw, lane); cstage<T2, 256, 8, 8>(lA, sB, tw, lane);
+    cstage<T2, 256, 4, 64>(lB, st, tw, lane);
+  } else if constexpr (N == 512) {
+    cstage<T2, 512, 8, 1>(ld, sA, tw, lane); cstage<T2, 512, 8, 8>(lA, sB, tw, lane);
+    cstage<T2, 512, 8, 64>(lB, st, tw, lane);
+  } else if constexpr (N == 1024) {
+    cstage<T2, 1024, 8, 1>(ld, sA, tw, lane); cstage<T2, 1024, 8, 8>(lA, sB, tw, lane);
+    cstage<T2, 1024, 4, 64>(lB, sA, tw, lane); cstage<T2, 1024, 4, 256>(lA, st, tw, lane);
+  } else {
+    static_assert(N == 64, "unsupported compile-time FFT size");
+  }
+}
+
+// Runtime mixed-radix (2,3,4,5,8) version for sizes without a compile-time path (e.g. 720, 1440).
+template <typename T2, int R, class Ld, class St>
+__device__ __forceinline__ void rstage(Ld ld, St st, int N, int Ns, const T2* __restrict__ tw, int lane) {
+  const int NB = N / R, step = N / (Ns * R);
+  for (int j = lane; j < NB; j += 32) {
+    T2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = ld(j + r * NB);
+    const int jm = j % Ns;
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[jm * step * r]);
+    Dft<T2, R>::run(v);
+    const int idxD = (j - jm) * R + jm;
+#pragma unroll
+    for (int r = 0; r < R; ++r) st(idxD + r * Ns, v[r]);
+  }
+  __syncwarp();
+}
+
+template <typename T2, class Ld, class St>
+__device__ __forceinline__ void rstage_any(int R, Ld ld, St st, int N, int Ns, const T2* tw, int lane) {
   switch (R) {
-    case 8: fft_stage<T2, 8>(src, sst, dst, dstr, N, Ns, tw, lane); break;
-    case 4: fft_stage<T2, 4>(src, sst, dst, dstr, N, Ns, tw, lane); break;
-    case 2: fft_stage<T2, 2>(src, sst, dst, dstr, N, Ns, tw, lane); break;
-    case 5: fft_stage<T2, 5>(src, sst, dst, dstr, N, Ns, tw, lane); break;
-    default: fft_stage<T2, 3>(src, sst, dst, dstr, N, Ns, tw, lane); break;
+    case 8: rstage<T2, 8>(ld, st, N, Ns, tw, lane); break;
+    case 4: rstage<T2, 4>(ld, st, N, Ns, tw, lane); break;
+    case 2: rstage<T2, 2>(ld, st, N, Ns, tw, lane); break;
+    case 5: rstage<T2, 5>(ld, st, N, Ns, tw, lane); break;
+    default: rstage<T2, 3>(ld, st, N, Ns, tw, lane); break;
   }
 }
 
-// Length-N forward FFT by one warp with ping-pong buffers A, B (stride 1, N complex each).
-// out == nullptr: the input must be in A; the result is left in A or B and its pointer returned.
-// out != nullptr: input `in` (stride ist) -> output `out` (stride ost); needs >= 2 stages.
-template <typename T2>
-__device__ T2* warp_fft(const T2* in, int ist, T2* out, int ost, T2* A, T2* B, const FftPlan& f, const T2* tw,
-                        int lane) {
-  int Ns = 1;
+template <typename T2, class Ld, class St>
+__device__ void fft_rt(const FftPlan& f, Ld ld, St st, T2* A, T2* B, const T2* tw, int lane) {
+  auto lA = [A](int i) { return A[i]; };
+  auto lB = [B](int i) { return B[i]; };
+  auto sA = [A](int i, T2 v) { A[i] = v; };
+  auto sB = [B](int i, T2 v) { B[i] = v; };
   const int last = f.nstages - 1;
-  if (out == nullptr) {
-    for (int s = 0; s <= last; ++s) {
-      const T2* src = (s & 1) ? B : A;
-      T2* dst = (s & 1) ? A : B;
-      fft_stage_any<T2>(f.radix[s], src, 1, dst, 1, f.n, Ns, tw, lane);
-      Ns *= f.radix[s];
-    }
-    return (f.nstages & 1) ? B : A;
-  }
+  int Ns = 1;
   for (int s = 0; s <= last; ++s) {
-    const T2* src = (s == 0) ? in : ((s - 1) & 1 ? B : A);
-    const int sst = (s == 0) ? ist : 1;
-    T2* dst = (s == last) ? out : ((s & 1) ? B : A);
-    const int dstr = (s == last) ? ost : 1;
-    fft_stage_any<T2>(f.radix[s], src, sst, dst, dstr, f.n, Ns, tw, lane);
-    Ns *= f.radix[s];
+    const int R = f.radix[s];
+    const bool in_A = (s & 1);          // stage s >= 1 reads the buffer written by stage s-1
+    if (s == 0 && s == last) rstage_any<T2>(R, ld, st, f.n, Ns, tw, lane);
+    else if (s == 0) rstage_any<T2>(R, ld, sA, f.n, Ns, tw, lane);
+    else if (s == last) { if (in_A) rstage_any<T2>(R, lA, st, f.n, Ns, tw, lane); else rstage_any<T2>(R, lB, st, f.n, Ns, tw, lane); }
+    else { if (in_A) rstage_any<T2>(R, lA, sB, f.n, Ns, tw, lane); else rstage_any<T2>(R, lB, sA, f.n, Ns, tw, lane); }
+    Ns *= R;
   }
-  return out;
 }
 
-template <typename T> __device__ __forceinline__ T es_weight(T d, T inv_hw, T beta);
-template <> __device__ __forceinline__ float es_weight<float>(float d, float inv_hw, float beta) {
-  float z = d * inv_hw;
-  float s = sqrtf(fmaxf(0.f, 1.f - z * z));
-  return __expf(beta * (s - 1.f));
-}
-template <> __device__ __forceinline__ double es_weight<double>(double d, double inv_hw, double beta) {
-  double z = d * inv_hw;
-  double s = sqrt(fmax(0.0, 1.0 - z * z));
-  return exp(beta * (s - 1.0));
+template <typename T2, int NC, class Ld, class St>
+__device__ __forceinline__ void fft_any(const FftPlan& f, Ld ld, St st, T2* A, T2* B, const T2* tw, int lane) {
+  if constexpr (NC > 0) fft_pow2<T2, NC>(ld, st, A, B, tw, lane);
+  else fft_rt<T2>(f, ld, st, A, B, tw, lane);
 }
 
-template <typename T, int W>
+// ---------------------------------------------------------------- ES window weights
+// phi(d) = exp(beta (sqrt(1 - (d/hw)^2) - 1)), |d| <= hw.  fp32: MUFU sqrt.approx / ex2.approx
+// (relative error ~1e-7, far below the 1e-5 NUFFT budget); fp64: exact.
+__device__ __forceinline__ float sqrt_approx(float x) { float y; asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ float ex2_approx(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+
+template <typename T> struct Es;
+template <> struct Es<float> {
+  float inv_hw, bl;                       // bl = beta * log2(e)
+  __device__ Es(double hw, double beta) : inv_hw(float(1.0 / hw)), bl(float(beta * 1.4426950408889634)) {}
+  __device__ __forceinline__ float operator()(float d) const {
+    const float z = d * inv_hw;
+    const float s = sqrt_approx(fmaxf(fmaf(-z, z, 1.f), 0.f));
+    return ex2_approx(fmaf(s, bl, -bl));
+  }
+};
+template <> struct Es<double> {
+  double inv_hw, beta;
+  __device__ Es(double hw, double b) : inv_hw(1.0 / hw), beta(b) {}
+  __device__ __forceinline__ double operator()(double d) const {
+    const double z = d * inv_hw;
+    return exp(beta * (sqrt(fmax(1.0 - z * z, 0.0)) - 1.0));
+  }
+};
+
+// ---------------------------------------------------------------- the fused polar kernel
+// MC: compile-time M (0 = runtime plan); when MC > 0 the ring FFT length is 2 MC.
+template <typename T, int W, int MC>
 __global__ void __launch_bounds__(512, 1)
 polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, int64_t n_img, int64_t img_stride,
              T* __restrict__ ghat) {
   using T2 = typename Cx<T>::t;
+  constexpr int NC = MC > 0 ? 2 * MC : 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PolarParams& pp = *reinterpret_cast<PolarParams*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x, nwarps = nthr >> 5;
@@ -178,18 +239,18 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
     for (int i = tid; i < (int)(sizeof(PolarParams) / 4); i += nthr) dst[i] = src[i];
   }
   __syncthreads();
-  const int M = pp.M, L = pp.L, nt = pp.n_theta, half = pp.half, n_xi = pp.n_xi;
+  const int M = MC > 0 ? MC : pp.M;
+  const int L = pp.L, nt = MC > 0 ? NC : pp.n_theta, half = nt / 2, n_xi = pp.n_xi;
   unsigned char* base = smem_raw + ((sizeof(PolarParams) + 15) / 16) * 16;
   T2* twM = reinterpret_cast<T2*>(base);
   T2* twT = twM + M;
   T* dap = reinterpret_cast<T*>(twT + nt);
   T2* wscr = reinterpret_cast<T2*>(base + (((size_t)(M + nt) * sizeof(T2) + (size_t)L * sizeof(T) + 15) / 16) * 16);
-  T2* region = wscr + (size_t)nwarps * 2 * M;
+  T2* region = wscr + (size_t)pp.fft_warps * 2 * M;
   T2* myA = wscr + (size_t)warp * 2 * M;          // row / column FFT ping-pong
   T2* myB = myA + M;
   T2* angA = region + (size_t)warp * 2 * nt;      // angular FFT ping-pong (region is free then)
   T2* angB = angA + nt;
-
   {
     const T2* gtM = reinterpret_cast<const T2*>(pp.tw_M);
     const T2* gtT = reinterpret_cast<const T2*>(pp.tw_theta);
@@ -203,62 +264,80 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
   T2* X = reinterpret_cast<T2*>(pp.xscratch) + (int64_t)blockIdx.x * pp.xscratch_stride;
   T2* Pol = reinterpret_cast<T2*>(pp.pscratch) + (int64_t)blockIdx.x * pp.pscratch_stride;
   const int ncx = pp.ncols_x, col_lo = pp.col_lo, S = pp.S;
-  const int kk = (pp.k_max + 1) | 1;
-  const T hw = T(pp.half_w), inv_hw = T(1) / hw, beta = T(pp.beta);
+  const int PADR = W;                              // wrapped duplicate rows on each side
+  const int row0 = M / 2 + PADR;                   // physical row of m1 = 0
+  const Es<T> phi(pp.half_w, pp.beta);
+  const int G = pp.ring_group;
 
   for (int64_t img = blockIdx.x; img < n_img; img += gridDim.x) {
     const T* I = images + img * img_stride;
-    // ---------------- K1a: row FFTs (pairs of real rows packed as one complex sequence) ----------------
-    for (int pr = warp; pr < (L + 1) / 2; pr += nwarps) {
-      T2* sc = myA;
-      for (int t = lane; t < M; t += 32) sc[t] = T2{T(0), T(0)};
-      __syncwarp();
-      const int a0 = 2 * pr, a1 = a0 + 1;
-      const bool has1 = a1 < L;
-      const T d0 = dap[a0], d1 = has1 ? dap[a1] : T(0);
-      for (int b = lane; b < L; b += 32) {
-        int pos = b - L / 2; if (pos < 0) pos += M;
-        T v0 = I[(int64_t)a0 * L + b] * d0 * dap[b];
-        T v1 = has1 ? I[(int64_t)a1 * L + b] * d1 * dap[b] : T(0);
-        sc[pos] = T2{v0, v1};
+    // ---------------- K1a: row FFTs, two real rows per complex sequence, deapodised + zero-padded on load
+    if (warp < pp.fft_warps) {
+      for (int pr = warp; pr < (L + 1) / 2; pr += pp.fft_warps) {
+        const int a0 = 2 * pr, a1 = a0 + 1;
+        const bool has1 = a1 < L;
+        const T* r0 = I + (int64_t)a0 * L;
+        const T* r1 = I + (int64_t)(has1 ? a1 : a0) * L;
+        const T d0 = dap[a0], d1 = has1 ? dap[a1] : T(0);
+        auto ld = [&](int t) -> T2 {
+          const int b = (t < M / 2 ? t : t - M) + L / 2;          // pixel column of FFT position t
+          if (b < 0 || b >= L) return T2{T(0), T(0)};
+          const T db = dap[b];
+          return T2{__ldg(r0 + b) * d0 * db, __ldg(r1 + b) * d1 * db};
+        };
+        T2* res = region + (size_t)warp * M;                         // the phase region is free here
+        auto st = [res](int i, T2 v) { res[i] = v; };
+        fft_any<T2, MC>(pp.fft_M, ld, st, myA, myB, twM, lane);
+        for (int cc = lane; cc < ncx; cc += 32) {
+          int m = (col_lo + cc) % M; if (m < 0) m += M;
+          int mm = M - m; if (mm == M) mm = 0;
+          T2 zm = res[m], zc = res[mm];
+          zc.y = -zc.y;                                              // conj Z(-m)
+          const T2 xa = {T(0.5) * (zm.x + zc.x), T(0.5) * (zm.y + zc.y)};
+          const T2 dd = csub(zm, zc);
+          const T2 xb = {T(0.5) * dd.y, T(-0.5) * dd.x};             // (Z(m) - conj Z(-m)) / (2i)
+          X[(int64_t)a0 * ncx + cc] = xa;
+          if (has1) X[(int64_t)a1 * ncx + cc] = xb;
+        }
+        __syncwarp();
       }
-      __syncwarp();
-      sc = warp_fft<T2>(myA, 1, nullptr, 1, myA, myB, pp.fft_M, twM, lane);
-      for (int cc = lane; cc < ncx; cc += 32) {
-        int m = (col_lo + cc) % M; if (m < 0) m += M;
-        int mm = M - m; if (mm == M) mm = 0;
-        T2 zm = sc[m], zc = sc[mm];
-        zc.y = -zc.y;                                          // conj Z(-m)
-        T2 xa = {T(0.5) * (zm.x + zc.x), T(0.5) * (zm.y + zc.y)};
-        T2 dd = csub(zm, zc);
-        T2 xb = {T(0.5) * dd.y, T(-0.5) * dd.x};               // (Z(m) - conj Z(-m)) / (2i)
-        X[(int64_t)a0 * ncx + cc] = xa;
-        if (has1) X[(int64_t)a1 * ncx + cc] = xb;
-      }
-      __syncwarp();
     }
     __syncthreads();
 
-    // ---------------- per phase: K1b column FFTs in shared memory, K2 gather ----------------
+    // ---------------- per phase: K1b column FFTs (input rows 0..L-1 = image rows, output fftshifted with
+    // PADR wrapped duplicate rows), then K2 gather of node pairs (theta, pi - theta)
     for (int ph = 0; ph < pp.n_phase; ++ph) {
       const int lo = pp.phase_lo[ph];
       int ncols = col_lo + ncx - lo; if (ncols > S) ncols = S;
       T2* Gc = region;
-      for (int idx = tid; idx < M * ncols; idx += nthr) {
-        const int row = idx / ncols, cc = idx - row * ncols;
-        const int i1 = row < M / 2 ? row : row - M;
-        const int a = i1 + L / 2;
-        T2 v = T2{T(0), T(0)};
-        if (a >= 0 && a < L) v = X[(int64_t)a * ncx + (lo - col_lo) + cc];
-        Gc[row * S + cc] = v;
+      for (int a = warp; a < L; a += nwarps) {
+        const T2* src = X + (int64_t)a * ncx + (lo - col_lo);
+        T2* dst = Gc + (size_t)a * S;
+        for (int cc = lane; cc < ncols; cc += 32) dst[cc] = src[cc];
       }
       __syncthreads();
-      for (int cc = warp; cc < ncols; cc += nwarps) warp_fft<T2>(Gc + cc, S, Gc + cc, S, myA, myB, pp.fft_M, twM, lane);
+      if (warp < pp.fft_warps) {
+        for (int cc = warp; cc < ncols; cc += pp.fft_warps) {
+          T2* col = Gc + cc;
+          auto ld = [&](int t) -> T2 {
+            const int a = (t < M / 2 ? t : t - M) + L / 2;
+            return (a >= 0 && a < L) ? col[(size_t)a * S] : T2{T(0), T(0)};
+          };
+          auto st = [&](int t, T2 v) {
+            const int m1 = t < M / 2 ? t : t - M;
+            col[(size_t)(m1 + row0) * S] = v;
+            if (m1 < -M / 2 + PADR) col[(size_t)(m1 + M + row0) * S] = v;
+            if (m1 >= M / 2 - PADR) col[(size_t)(m1 - M + row0) * S] = v;
+          };
+          fft_any<T2, MC>(pp.fft_M, ld, st, myA, myB, twM, lane);
+        }
+      }
       __syncthreads();
       const int nb = pp.phase_node_begin[ph], ne = pp.phase_node_begin[ph + 1];
       for (int t = nb + tid; t < ne; t += nthr) {
         const uint32_t nd = __ldg(pp.nodes + t);
         const int j = int(nd >> 16), l = int(nd & 0xffffu);
+        const bool pair = (l != 0) && (2 * l != half);
         const double r = __ldg(pp.rho + j);
         const double k1 = r * __ldg(pp.cs + 2 * l), k2 = r * __ldg(pp.cs + 2 * l + 1);
         const double f1 = ceil(k1 - pp.half_w), f2 = ceil(k2 - pp.half_w);
@@ -266,54 +345,59 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         const T t1 = T(k1 - f1), t2 = T(k2 - f2);
         T wx[W], wy[W];
 #pragma unroll
-        for (int q = 0; q < W; ++q) {
-          wx[q] = es_weight<T>(t1 - T(q), inv_hw, beta);
-          wy[q] = es_weight<T>(t2 - T(q), inv_hw, beta);
-        }
-        T2 acc = T2{T(0), T(0)};
+        for (int q = 0; q < W; ++q) { wx[q] = phi(t1 - T(q)); wy[q] = phi(t2 - T(q)); }
         const T2* gcol = Gc + (b2 - lo);
+        T2 accA = T2{T(0), T(0)}, accB = T2{T(0), T(0)};
 #pragma unroll
         for (int q = 0; q < W; ++q) {
-          int row = b1 + q;
-          row = row < 0 ? row + M : (row >= M ? row - M : row);
-          const T2* gp = gcol + row * S;
-          T2 s = T2{T(0), T(0)};
+          const T2* ga = gcol + (size_t)(b1 + q + row0) * S;        // node (k1, k2)
+          const T2* gb = gcol + (size_t)(row0 - b1 - q) * S;        // node (-k1, k2), mirrored taps
+          T2 sa = T2{T(0), T(0)}, sb = T2{T(0), T(0)};
 #pragma unroll
           for (int c = 0; c < W; ++c) {
-            const T2 g = gp[c];
-            s.x += wy[c] * g.x; s.y += wy[c] * g.y;
+            const T2 g = ga[c];
+            sa.x += wy[c] * g.x; sa.y += wy[c] * g.y;
           }
-          acc.x += wx[q] * s.x; acc.y += wx[q] * s.y;
+          if (pair) {
+#pragma unroll
+            for (int c = 0; c < W; ++c) {
+              const T2 g = gb[c];
+              sb.x += wy[c] * g.x; sb.y += wy[c] * g.y;
+            }
+          }
+          accA.x += wx[q] * sa.x; accA.y += wx[q] * sa.y;
+          accB.x += wx[q] * sb.x; accB.y += wx[q] * sb.y;
         }
-        Pol[(int64_t)j * half + l] = acc;
+        Pol[(int64_t)j * half + l] = accA;
+        if (pair) Pol[(int64_t)j * half + (half - l)] = accB;
       }
       __syncthreads();
     }
 
-    // ---------------- K3: angular FFT per ring, staged, written k-major ----------------
-    const int G = pp.ring_group;
+    // ---------------- K3: ring FFTs (full ring rebuilt from the half ring), staged [k][jj], written k-major
+    T2* stg = region + (size_t)pp.ang_warps * 2 * nt;
     for (int j0 = 0; j0 < n_xi; j0 += G) {
       const int g = min(G, n_xi - j0);
-      T2* stg = region + (size_t)nwarps * 2 * nt;
-      for (int jj = warp; jj < g; jj += nwarps) {
-        T2* sc = angA;
-        const T2* src = Pol + (int64_t)(j0 + jj) * half;
-        for (int l = lane; l < half; l += 32) {
-          T2 v = src[l];
-          sc[l] = v;
-          sc[l + half] = T2{v.x, -v.y};
+      if (warp < pp.ang_warps) {
+        for (int jj = warp; jj < g; jj += pp.ang_warps) {
+          const T2* src = Pol + (int64_t)(j0 + jj) * half;
+          auto ld = [&](int t) -> T2 {
+            if (t < half) return src[t];
+            const T2 v = src[t - half];
+            return T2{v.x, -v.y};
+          };
+          const int kmx = pp.k_max;
+          auto st = [&](int t, T2 v) { if (t <= kmx) stg[(size_t)t * G + jj] = v; };
+          fft_any<T2, NC>(pp.fft_theta, ld, st, angA, angB, twT, lane);
         }
-        __syncwarp();
-        sc = warp_fft<T2>(angA, 1, nullptr, 1, angA, angB, pp.fft_theta, twT, lane);
-        for (int k = lane; k <= pp.k_max; k += 32) stg[jj * kk + k] = sc[k];
-        __syncwarp();
       }
       __syncthreads();
-      const int tot = (pp.k_max + 1) * 2 * g;
-      for (int idx = tid; idx < tot; idx += nthr) {
-        const int jj = idx % g, rest = idx / g, part = rest & 1, k = rest >> 1;
-        const T2 v = stg[jj * kk + k];
-        ghat[(((int64_t)k * n_img + img) * 2 + part) * n_xi + j0 + jj] = part ? v.y : v.x;
+      const int rows = (pp.k_max + 1) * 2;
+      for (int rw = warp; rw < rows; rw += nwarps) {
+        const int k = rw >> 1, part = rw & 1;
+        T* dst = ghat + (((int64_t)k * n_img + img) * 2 + part) * n_xi + j0;
+        const T2* sp = stg + (size_t)k * G;
+        for (int jj = lane; jj < g; jj += 32) dst[jj] = part ? sp[jj].y : sp[jj].x;
       }
       __syncthreads();
     }
@@ -327,10 +411,10 @@ int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps) {
          nwarps * 2 * M * csz;
 }
 
-template <typename T, int W>
+template <typename T, int W, int MC>
 static cudaError_t launch_polar_t(const Plan& P, const void* d_images, int64_t n_img, int64_t stride,
                                   cudaStream_t s) {
-  auto kern = polar_kernel<T, W>;
+  auto kern = polar_kernel<T, W, MC>;
   static int configured = 0;
   if (configured < P.polar_smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P.polar_smem);
@@ -344,14 +428,24 @@ static cudaError_t launch_polar_t(const Plan& P, const void* d_images, int64_t n
 }
 
 cudaError_t launch_polar(const Plan& P, const void* d_images, int64_t n_img, int64_t stride, cudaStream_t s) {
+  const bool pow2 = P.n_theta == 2 * P.M && (P.M == 64 || P.M == 128 || P.M == 256 || P.M == 512);
   if (P.dt == FBSPCA_F64) {
     if (P.w != 13) return cudaErrorInvalidValue;
-    return launch_polar_t<double, 13>(P, d_images, n_img, stride, s);
+    if (pow2 && P.M == 64) return launch_polar_t<double, 13, 64>(P, d_images, n_img, stride, s);
+    return launch_polar_t<double, 13, 0>(P, d_images, n_img, stride, s);
+  }
+  if (P.w == 6 && pow2) {
+    switch (P.M) {
+      case 128: return launch_polar_t<float, 6, 128>(P, d_images, n_img, stride, s);
+      case 256: return launch_polar_t<float, 6, 256>(P, d_images, n_img, stride, s);
+      case 512: return launch_polar_t<float, 6, 512>(P, d_images, n_img, stride, s);
+      default: break;
+    }
   }
   switch (P.w) {
-    case 6: return launch_polar_t<float, 6>(P, d_images, n_img, stride, s);
-    case 7: return launch_polar_t<float, 7>(P, d_images, n_img, stride, s);
-    case 8: return launch_polar_t<float, 8>(P, d_images, n_img, stride, s);
+    case 6: return launch_polar_t<float, 6, 0>(P, d_images, n_img, stride, s);
+    case 7: return launch_polar_t<float, 7, 0>(P, d_images, n_img, stride, s);
+    case 8: return launch_polar_t<float, 8, 0>(P, d_images, n_img, stride, s);
     default: return cudaErrorInvalidValue;
   }
 }

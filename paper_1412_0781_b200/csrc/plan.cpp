@@ -209,21 +209,26 @@ fbspca_status build_host_plan(Plan& P) {
   if (pp.fft_M.nstages < 0 || pp.fft_theta.nstages < 0) { set_error("FFT sizes must be 2^a 3^b 5^c"); return FBSPCA_ERR_CONFIG; }
   pp.nwarps = 16;
   const int csz = (P.dt == FBSPCA_F32) ? 8 : 16;       // sizeof complex
-  const int fixed = polar_fixed_smem(M, P.n_theta, L, csz, pp.nwarps);
-  const int budget = polar_max_smem() - fixed;
+  const int cap = polar_max_smem();
+  pp.fft_warps = 16;
+  while (pp.fft_warps > 2 && pp.fft_warps * 2 * M * csz > cap / 3) pp.fft_warps /= 2;
+  const int fixed = polar_fixed_smem(M, P.n_theta, L, csz, pp.fft_warps);
+  const int budget = cap - fixed;
   const int kk = (P.k_max + 1) | 1;                    // staging row stride (odd)
-  const int ang_scr = pp.nwarps * 2 * P.n_theta * csz;
-  if (budget < ang_scr + kk * csz || budget < M * 11 * csz) {
+  pp.ang_warps = std::min(16, (budget - kk * csz) / (2 * P.n_theta * csz));
+  if (pp.ang_warps < 1 || budget < M * 11 * csz) {
     set_error("image too large for the fused polar kernel's shared memory"); return FBSPCA_ERR_CONFIG;
   }
-  int S = budget / (M * csz);
+  const int ang_scr = pp.ang_warps * 2 * P.n_theta * csz;
+  const int rows_g = M + 2 * w;                          // Gc rows incl. wrapped duplicates (PADR = w)
+  int S = budget / (rows_g * csz);
   if (S % 2 == 0) --S;                                   // odd row stride (bank spread)
   if (S > pp.ncols_x) S = pp.ncols_x | 1;
   pp.S = S;
   int G = (budget - ang_scr) / (kk * csz);
   G = std::max(1, std::min(G, std::min(32, P.n_xi)));
   pp.ring_group = G;
-  const int region = std::max(M * S * csz, ang_scr + G * kk * csz);
+  const int region = std::max(std::max(rows_g * S * csz, pp.fft_warps * M * csz), ang_scr + G * kk * csz);
   pp.smem_region_bytes = region;
   P.polar_smem = fixed + region;
   // phases over columns: phase p holds m2 in [lo_p, lo_p + S) and owns nodes with b2 in [lo_p, lo_p + S - w]
@@ -241,7 +246,8 @@ fbspca_status build_host_plan(Plan& P) {
     while (pos < order.size() && b2[order[pos]] <= lo + S - w) {
       int id = order[pos++];
       int j = id / half, l = id % half;
-      ph.push_back((uint32_t(j) << 16) | uint32_t(l));
+      // pair leaders only: node (j, half - l) = (-k1, k2) is gathered with (j, l) (same columns)
+      if (2 * l <= half) ph.push_back((uint32_t(j) << 16) | uint32_t(l));
     }
     std::sort(ph.begin(), ph.end());                      // ring-major within a phase
     P.nodes.insert(P.nodes.end(), ph.begin(), ph.end());
