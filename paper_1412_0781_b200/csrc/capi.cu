@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -125,6 +126,18 @@ fbspca_status upload_plan(Plan& P) {
   if (f32) {
     auto tab = cast_vec<float>(P.table);
     FB_CUDA(upload(&P.d_table, tab.data(), tab.size()), "upload table");
+    std::vector<float> hi(tab.size()), lo(tab.size());
+    for (size_t i = 0; i < tab.size(); ++i) {          // tf32 round-to-nearest (ties away), as cvt.rna.tf32
+      uint32_t b;
+      std::memcpy(&b, &tab[i], 4);
+      b = (b + 0x1000u) & ~0x1FFFu;
+      std::memcpy(&hi[i], &b, 4);
+      lo[i] = tab[i] - hi[i];
+    }
+    FB_CUDA(upload((void**)&P.d_table_hi, hi.data(), hi.size()), "upload table hi");
+    FB_CUDA(upload((void**)&P.d_table_lo, lo.data(), lo.size()), "upload table lo");
+    const char* k4 = getenv("FBSPCA_K4");
+    P.use_tc = !(k4 && std::string(k4) == "simt");
     auto dp = cast_vec<float>(P.deapod);
     FB_CUDA(upload(&P.d_deapod, dp.data(), dp.size()), "upload deapod");
     auto tm = twiddles<float2, float>(P.M);
@@ -170,7 +183,7 @@ void free_plan(Plan& P) {
   DeviceGuard g(P.device);
   void* ptrs[] = {P.d_table, P.d_deapod, P.d_tw_M, P.d_tw_theta, P.d_rho, P.d_cs, P.d_nodes, P.d_xscratch,
                   P.d_pscratch, P.d_ghat, P.d_partial, P.d_p, P.d_coef_off, P.d_blk_off, P.d_evec_off,
-                  P.d_eig_work, P.d_eig_sweeps, P.d_coef_k, P.d_pp, P.d_cov_scratch};
+                  P.d_eig_work, P.d_eig_sweeps, P.d_coef_k, P.d_pp, P.d_cov_scratch, P.d_table_hi, P.d_table_lo};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& ev : P.tevents) { cudaEventDestroy(ev.second.first); cudaEventDestroy(ev.second.second); }
 }
@@ -257,7 +270,8 @@ fbspca_status fbspca_expand(fbspca_plan_t h, const void* d_images, int64_t n, vo
     }
     {
       TimedRegion t(P, T_RADIAL, s);
-      FB_CUDA(launch_radial(P, nb, b0, n, d_coeffs, s), "radial kernel");
+      if (P.dt == FBSPCA_F32 && P.use_tc && P.n_xi % 4 == 0) FB_CUDA(launch_radial_tc(P, nb, b0, n, d_coeffs, s), "radial tc kernel");
+      else FB_CUDA(launch_radial(P, nb, b0, n, d_coeffs, s), "radial kernel");
     }
   }
   return FBSPCA_OK;

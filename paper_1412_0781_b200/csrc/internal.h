@@ -82,6 +82,9 @@ struct Plan {
   int polar_grid = 0;                    // resident CTAs of the polar kernel
   // device buffers
   void* d_table = nullptr;               // T (float or double), coef rows x n_xi
+  float* d_table_lo = nullptr;           // fp32 plans: T - tf32(T)  (3xTF32 tensor-core K4)
+  float* d_table_hi = nullptr;           // fp32 plans: tf32_rna(T)
+  bool use_tc = true;                    // K4 on tcgen05 (fp32 plans)
   void* d_deapod = nullptr;
   void* d_tw_M = nullptr;
   void* d_tw_theta = nullptr;
@@ -129,6 +132,7 @@ cudaError_t launch_project(const Plan& P, const void* d_coeffs, int64_t n, const
                            const double* d_evals, const double* d_evecs, double sigma2, int mode,
                            int64_t n_total, void* d_out, cudaStream_t s);
 int polar_max_smem();
+cudaError_t launch_radial_tc(const Plan& P, int64_t nb, int64_t i0, int64_t ld, void* d_coeffs, cudaStream_t s);
 int fft_values_per_lane(const FftPlan& f);
 int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps);
 

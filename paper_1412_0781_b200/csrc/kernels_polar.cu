@@ -117,12 +117,16 @@ __device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tw, 
 }
 
 // Compile-time power-of-two FFT: first stage reads ld(), last stage writes st(), ping-pong in A, B.
+// Ping-pong scratch index with one pad element per 16 (breaks the 4-way bank conflicts of Ns = 8 stores).
+__device__ __forceinline__ int padi(int i) { return i + (i >> 4); }
+template <int N> constexpr int padded_len() { return N + N / 16; }
+
 template <typename T2, int N, class Ld, class St>
 __device__ __forceinline__ void fft_pow2(Ld ld, St st, T2* A, T2* B, const T2* tw, int lane) {
-  auto lA = [A](int i) { return A[i]; };
-  auto lB = [B](int i) { return B[i]; };
-  auto sA = [A](int i, T2 v) { A[i] = v; };
-  auto sB = [B](int i, T2 v) { B[i] = v; };
+  auto lA = [A](int i) { return A[padi(i)]; };
+  auto lB = [B](int i) { return B[padi(i)]; };
+  auto sA = [A](int i, T2 v) { A[padi(i)] = v; };
+  auto sB = [B](int i, T2 v) { B[padi(i)] = v; };
   if constexpr (N == 64) {
     cstage<T2, 64, 8, 1>(ld, sA, tw, lane); cstage<T2, 64, 8, 8>(lA, st, tw, lane);
   } else if constexpr (N == 128) {
@@ -174,10 +178,10 @@ __device__ __forceinline__ void rstage_any(int R, Ld ld, St st, int N, int Ns, c
 
 template <typename T2, class Ld, class St>
 __device__ void fft_rt(const FftPlan& f, Ld ld, St st, T2* A, T2* B, const T2* tw, int lane) {
-  auto lA = [A](int i) { return A[i]; };
-  auto lB = [B](int i) { return B[i]; };
-  auto sA = [A](int i, T2 v) { A[i] = v; };
-  auto sB = [B](int i, T2 v) { B[i] = v; };
+  auto lA = [A](int i) { return A[padi(i)]; };
+  auto lB = [B](int i) { return B[padi(i)]; };
+  auto sA = [A](int i, T2 v) { A[padi(i)] = v; };
+  auto sB = [B](int i, T2 v) { B[padi(i)] = v; };
   const int last = f.nstages - 1;
   int Ns = 1;
   for (int s = 0; s <= last; ++s) {
@@ -246,11 +250,12 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
   T2* twT = twM + M;
   T* dap = reinterpret_cast<T*>(twT + nt);
   T2* wscr = reinterpret_cast<T2*>(base + (((size_t)(M + nt) * sizeof(T2) + (size_t)L * sizeof(T) + 15) / 16) * 16);
-  T2* region = wscr + (size_t)pp.fft_warps * 2 * M;
-  T2* myA = wscr + (size_t)warp * 2 * M;          // row / column FFT ping-pong
-  T2* myB = myA + M;
-  T2* angA = region + (size_t)warp * 2 * nt;      // angular FFT ping-pong (region is free then)
-  T2* angB = angA + nt;
+  const int MP = M + M / 16, NTP = nt + nt / 16;  // padded ping-pong lengths (padi)
+  T2* region = wscr + (size_t)pp.fft_warps * 2 * MP;
+  T2* myA = wscr + (size_t)warp * 2 * MP;         // row / column FFT ping-pong
+  T2* myB = myA + MP;
+  T2* angA = region + (size_t)warp * 2 * NTP;     // angular FFT ping-pong (region is free then)
+  T2* angB = angA + NTP;
   {
     const T2* gtM = reinterpret_cast<const T2*>(pp.tw_M);
     const T2* gtT = reinterpret_cast<const T2*>(pp.tw_theta);
@@ -375,7 +380,8 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
     }
 
     // ---------------- K3: ring FFTs (full ring rebuilt from the half ring), staged [k][jj], written k-major
-    T2* stg = region + (size_t)pp.ang_warps * 2 * nt;
+    T2* stg = region + (size_t)pp.ang_warps * 2 * NTP;
+    const int GS = G | 1;                            // odd staging stride (bank spread)
     for (int j0 = 0; j0 < n_xi; j0 += G) {
       const int g = min(G, n_xi - j0);
       if (warp < pp.ang_warps) {
@@ -387,17 +393,25 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             return T2{v.x, -v.y};
           };
           const int kmx = pp.k_max;
-          auto st = [&](int t, T2 v) { if (t <= kmx) stg[(size_t)t * G + jj] = v; };
+          auto st = [&](int t, T2 v) { if (t <= kmx) stg[(size_t)t * GS + jj] = v; };
           fft_any<T2, NC>(pp.fft_theta, ld, st, angA, angB, twT, lane);
         }
       }
       __syncthreads();
-      const int rows = (pp.k_max + 1) * 2;
-      for (int rw = warp; rw < rows; rw += nwarps) {
-        const int k = rw >> 1, part = rw & 1;
-        T* dst = ghat + (((int64_t)k * n_img + img) * 2 + part) * n_xi + j0;
-        const T2* sp = stg + (size_t)k * G;
-        for (int jj = lane; jj < g; jj += 32) dst[jj] = part ? sp[jj].y : sp[jj].x;
+      {
+        // warp per k: lanes write rings j0 + lane (re row then im row), 128-B coalesced stores
+        const int64_t kstride = n_img * 2 * (int64_t)n_xi;
+        T* dst = ghat + img * 2 * (int64_t)n_xi + j0 + (int64_t)warp * kstride;
+        const T2* sp = stg + (size_t)warp * GS;
+        for (int k = warp; k <= pp.k_max; k += nwarps) {
+          for (int jj = lane; jj < g; jj += 32) {
+            const T2 v = sp[jj];
+            dst[jj] = v.x;
+            dst[jj + n_xi] = v.y;
+          }
+          dst += nwarps * kstride;
+          sp += (size_t)nwarps * GS;
+        }
       }
       __syncthreads();
     }
@@ -408,7 +422,7 @@ int polar_max_smem() { return 227 * 1024; }
 
 int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps) {
   return (int)(((sizeof(PolarParams) + 15) / 16) * 16) + (int)((((M + n_theta) * csz + L * (csz / 2)) + 15) / 16) * 16 +
-         nwarps * 2 * M * csz;
+         nwarps * 2 * (M + M / 16) * csz;
 }
 
 template <typename T, int W, int MC>

@@ -215,20 +215,22 @@ fbspca_status build_host_plan(Plan& P) {
   const int fixed = polar_fixed_smem(M, P.n_theta, L, csz, pp.fft_warps);
   const int budget = cap - fixed;
   const int kk = (P.k_max + 1) | 1;                    // staging row stride (odd)
-  pp.ang_warps = std::min(16, (budget - kk * csz) / (2 * P.n_theta * csz));
+  const int ntp = P.n_theta + P.n_theta / 16;          // padded ping-pong length
+  pp.ang_warps = std::min(8, (budget - 32 * kk * csz) / (2 * ntp * csz));
+  if (pp.ang_warps < 1) pp.ang_warps = std::min(8, (budget - kk * csz) / (2 * ntp * csz));
   if (pp.ang_warps < 1 || budget < M * 11 * csz) {
     set_error("image too large for the fused polar kernel's shared memory"); return FBSPCA_ERR_CONFIG;
   }
-  const int ang_scr = pp.ang_warps * 2 * P.n_theta * csz;
+  const int ang_scr = pp.ang_warps * 2 * ntp * csz;
   const int rows_g = M + 2 * w;                          // Gc rows incl. wrapped duplicates (PADR = w)
   int S = budget / (rows_g * csz);
   if (S % 2 == 0) --S;                                   // odd row stride (bank spread)
   if (S > pp.ncols_x) S = pp.ncols_x | 1;
   pp.S = S;
-  int G = (budget - ang_scr) / (kk * csz);
+  int G = (budget - ang_scr) / ((kk + 1) * csz) - 1;
   G = std::max(1, std::min(G, std::min(32, P.n_xi)));
   pp.ring_group = G;
-  const int region = std::max(std::max(rows_g * S * csz, pp.fft_warps * M * csz), ang_scr + G * kk * csz);
+  const int region = std::max(std::max(rows_g * S * csz, pp.fft_warps * M * csz), ang_scr + (G | 1) * kk * csz);
   pp.smem_region_bytes = region;
   P.polar_smem = fixed + region;
   // phases over columns: phase p holds m2 in [lo_p, lo_p + S) and owns nodes with b2 in [lo_p, lo_p + S - w]
