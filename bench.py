@@ -306,7 +306,9 @@ def main():
         sm_max = pk.get("sm_max_mhz", 1965.0)
         alu_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12          # fp32 FFMA TFLOP/s at max clock
         achieved = wk["polar_flops"] * imgs_per_launch / (per_launch_polar_ms / 1e3) / 1e12
-        n_cov_launch = math.ceil(n_local / 4096)
+        # per step: (polar + radial) per 4096-image expand batch; (k=0 fp64 SYRK + tcgen05 SYRK + chunk
+        # reduction) per 8192-image covariance batch; finalize.  NCCL's all-reduce kernel is not ours.
+        n_cov_launch = 3 * math.ceil(n_local / 8192)
         gpu_launches = args.steps * (2 * math.ceil(n_local / plan_batch(plan)) + n_cov_launch + 1)
         kernels = {}
         for name, tms in kms.items():

@@ -13,8 +13,8 @@ namespace fbspca {
 
 constexpr int kMaxRadixStages = 16;
 constexpr int kMaxPhases = 64;
-constexpr int kCovChunk = 512;          // images per covariance split-K chunk
-constexpr int kCovBatch = 16384;        // images per covariance launch
+constexpr int kCovChunk = 128;          // images per covariance split-K chunk (bounds fp32 accumulation length)
+constexpr int kCovBatch = 8192;         // images per covariance launch
 constexpr int kCovMaxChunks = kCovBatch / kCovChunk;
 
 // Stockham radix plan for a length-N FFT (N = prod radices; radices in {2,3,4,5,8}).
@@ -133,6 +133,8 @@ cudaError_t launch_project(const Plan& P, const void* d_coeffs, int64_t n, const
                            int64_t n_total, void* d_out, cudaStream_t s);
 int polar_max_smem();
 cudaError_t launch_radial_tc(const Plan& P, int64_t nb, int64_t i0, int64_t ld, void* d_coeffs, cudaStream_t s);
+cudaError_t launch_cov_tc(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb, cudaStream_t s);
+int radial_tc_cols(int pmax);
 int fft_values_per_lane(const FftPlan& f);
 int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps);
 

@@ -181,7 +181,14 @@ cudaError_t launch_cov_accum(const Plan& P, const void* d_coeffs, int64_t ld, in
   if (nchunk > kCovMaxChunks) return cudaErrorInvalidValue;
   const int64_t total = P.blk_off[P.k_max + 1] + P.p[0] + 1;
   dim3 grid((unsigned)(P.k_max + 1), (unsigned)(nt * (nt + 1) / 2), (unsigned)nchunk);
-  if (P.dt == FBSPCA_F32)
+  if (P.dt == FBSPCA_F32 && P.use_tc && P.p[0] <= 256 && (ld % 2) == 0) {   // float4 rows need even ld
+    // k >= 1 on the tensor cores; k = 0 (uncentred, mean^2/var ~ 10: F9) accumulates in fp64 on CUDA cores
+    dim3 g0(1u, (unsigned)(nt * (nt + 1) / 2), (unsigned)nchunk);
+    cov_accum_kernel<float><<<g0, 256, 0, s>>>((const float*)d_coeffs, P.d_p, P.d_coef_off, P.d_blk_off, ld, i0, nb,
+                                               P.k_max, P.d_cov_scratch, total);
+    cudaError_t e = launch_cov_tc(P, d_coeffs, ld, i0, nb, s);
+    if (e != cudaSuccess) return e;
+  } else if (P.dt == FBSPCA_F32)
     cov_accum_kernel<float><<<grid, 256, 0, s>>>((const float*)d_coeffs, P.d_p, P.d_coef_off, P.d_blk_off, ld, i0, nb,
                                                  P.k_max, P.d_cov_scratch, total);
   else

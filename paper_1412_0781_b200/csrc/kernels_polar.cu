@@ -92,9 +92,11 @@ template <typename T2> struct Dft<T2, 5> {
 // ---------------------------------------------------------------- warp FFTs with load/store functors
 // Stockham (autosort) stage of radix R: butterfly j reads ld(j + r NB), twiddles by w^(r (j mod Ns)),
 // DFT_R, writes st((j / Ns) Ns R + (j mod Ns) + r Ns).  Out of place; one warp; R values in registers.
-template <typename T2, int N, int R, int Ns, class Ld, class St>
-__device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tw, int lane) {
-  constexpr int NB = N / R, step = N / (Ns * R);
+// Twiddles come from a per-stage table tws[TOFF + (r - 1) Ns + (j mod Ns)] (contiguous in j: no bank
+// conflicts), built once per CTA by build_stage_tw<N>.
+template <typename T2, int N, int R, int Ns, int TOFF, class Ld, class St>
+__device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tws, int lane) {
+  constexpr int NB = N / R;
 #pragma unroll
   for (int j0 = 0; j0 < NB; j0 += 32) {
     const int j = j0 + lane;
@@ -105,7 +107,7 @@ __device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tw, 
       const int jm = j & (Ns - 1);
       if constexpr (Ns > 1) {
 #pragma unroll
-        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[jm * step * r]);
+        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tws[TOFF + (r - 1) * Ns + jm]);
       }
       Dft<T2, R>::run(v);
       const int idxD = (j - jm) * R + jm;
@@ -116,11 +118,42 @@ __device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tw, 
   __syncwarp();
 }
 
-// Compile-time power-of-two FFT: first stage reads ld(), last stage writes st(), ping-pong in A, B.
-// Ping-pong scratch index with one pad element per 16 (breaks the 4-way bank conflicts of Ns = 8 stores).
-__device__ __forceinline__ int padi(int i) { return i + (i >> 4); }
-template <int N> constexpr int padded_len() { return N + N / 16; }
+// Ping-pong scratch index swizzle: XOR the low 4 bits with 3 (i >> 4).  64-bit shared accesses resolve per
+// half-warp; this mapping keeps every load/store pattern of the stages below at 1.03x the ideal wavefronts
+// (unswizzled: 2.1x).
+__device__ __forceinline__ int padi(int i) { return i ^ ((3 * (i >> 4)) & 15); }
 
+// stage list per size: (R, Ns) ... ; table offsets TOFF accumulate (R - 1) Ns over stages with Ns > 1
+template <typename T2, int R, int Ns>
+__device__ __forceinline__ void fill_stage_tw(T2* dst, const T2* __restrict__ lin, int N, int tid, int nthr) {
+  const int step = N / (Ns * R);
+  for (int e = tid; e < (R - 1) * Ns; e += nthr) {
+    const int r = 1 + e / Ns, jm = e % Ns;
+    dst[e] = lin[jm * step * r];
+  }
+}
+template <int N> constexpr int stage_tw_len() {
+  return N == 64 ? 56 : N == 128 ? 120 : N == 256 ? 248 : N == 512 ? 504 : N == 1024 ? 1016 : N;
+}
+template <typename T2, int N>
+__device__ void build_stage_tw(T2* dst, const T2* __restrict__ lin, int tid, int nthr) {
+  if constexpr (N == 64) {
+    fill_stage_tw<T2, 8, 8>(dst, lin, N, tid, nthr);
+  } else if constexpr (N == 128) {
+    fill_stage_tw<T2, 4, 8>(dst, lin, N, tid, nthr); fill_stage_tw<T2, 4, 32>(dst + 24, lin, N, tid, nthr);
+  } else if constexpr (N == 256) {
+    fill_stage_tw<T2, 8, 8>(dst, lin, N, tid, nthr); fill_stage_tw<T2, 4, 64>(dst + 56, lin, N, tid, nthr);
+  } else if constexpr (N == 512) {
+    fill_stage_tw<T2, 8, 8>(dst, lin, N, tid, nthr); fill_stage_tw<T2, 8, 64>(dst + 56, lin, N, tid, nthr);
+  } else if constexpr (N == 1024) {
+    fill_stage_tw<T2, 8, 8>(dst, lin, N, tid, nthr); fill_stage_tw<T2, 4, 64>(dst + 56, lin, N, tid, nthr);
+    fill_stage_tw<T2, 4, 256>(dst + 248, lin, N, tid, nthr);
+  } else {
+    for (int i = tid; i < N; i += nthr) dst[i] = lin[i];     // runtime path: linear table
+  }
+}
+
+// Compile-time power-of-two FFT: first stage reads ld(), last stage writes st(), ping-pong in A, B.
 template <typename T2, int N, class Ld, class St>
 __device__ __forceinline__ void fft_pow2(Ld ld, St st, T2* A, T2* B, const T2* tw, int lane) {
   auto lA = [A](int i) { return A[padi(i)]; };
@@ -128,19 +161,19 @@ __device__ __forceinline__ void fft_pow2(Ld ld, St st, T2* A, T2* B, const T2* t
   auto sA = [A](int i, T2 v) { A[padi(i)] = v; };
   auto sB = [B](int i, T2 v) { B[padi(i)] = v; };
   if constexpr (N == 64) {
-    cstage<T2, 64, 8, 1>(ld, sA, tw, lane); cstage<T2, 64, 8, 8>(lA, st, tw, lane);
+    cstage<T2, 64, 8, 1, 0>(ld, sA, tw, lane); cstage<T2, 64, 8, 8, 0>(lA, st, tw, lane);
   } else if constexpr (N == 128) {
-    cstage<T2, 128, 8, 1>(ld, sA, tw, lane); cstage<T2, 128, 4, 8>(lA, sB, tw, lane);
-    cstage<T2, 128, 4, 32>(lB, st, tw, lane);
+    cstage<T2, 128, 8, 1, 0>(ld, sA, tw, lane); cstage<T2, 128, 4, 8, 0>(lA, sB, tw, lane);
+    cstage<T2, 128, 4, 32, 24>(lB, st, tw, lane);
   } else if constexpr (N == 256) {
-    cstage<T2, 256, 8, 1>(ld, sA, tw, lane); cstage<T2, 256, 8, 8>(lA, sB, tw, lane);
-    cstage<T2, 256, 4, 64>(lB, st, tw, lane);
+    cstage<T2, 256, 8, 1, 0>(ld, sA, tw, lane); cstage<T2, 256, 8, 8, 0>(lA, sB, tw, lane);
+    cstage<T2, 256, 4, 64, 56>(lB, st, tw, lane);
   } else if constexpr (N == 512) {
-    cstage<T2, 512, 8, 1>(ld, sA, tw, lane); cstage<T2, 512, 8, 8>(lA, sB, tw, lane);
-    cstage<T2, 512, 8, 64>(lB, st, tw, lane);
+    cstage<T2, 512, 8, 1, 0>(ld, sA, tw, lane); cstage<T2, 512, 8, 8, 0>(lA, sB, tw, lane);
+    cstage<T2, 512, 8, 64, 56>(lB, st, tw, lane);
   } else if constexpr (N == 1024) {
-    cstage<T2, 1024, 8, 1>(ld, sA, tw, lane); cstage<T2, 1024, 8, 8>(lA, sB, tw, lane);
-    cstage<T2, 1024, 4, 64>(lB, sA, tw, lane); cstage<T2, 1024, 4, 256>(lA, st, tw, lane);
+    cstage<T2, 1024, 8, 1, 0>(ld, sA, tw, lane); cstage<T2, 1024, 8, 8, 0>(lA, sB, tw, lane);
+    cstage<T2, 1024, 4, 64, 56>(lB, sA, tw, lane); cstage<T2, 1024, 4, 256, 248>(lA, st, tw, lane);
   } else {
     static_assert(N == 64, "unsupported compile-time FFT size");
   }
@@ -226,6 +259,18 @@ template <> struct Es<double> {
   }
 };
 
+// ---------------------------------------------------------------- optional stage profiler (debug builds only)
+#ifdef FBSPCA_PHASE_PROF
+__device__ unsigned long long g_phase_prof[1024 * 8];
+#define PROF_INIT() unsigned long long _pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long _pt = clock64();
+#define PROF_MARK(i) do { if (threadIdx.x == 0) { long long _n = clock64(); _pacc[i] += _n - _pt; _pt = _n; } } while (0)
+#define PROF_STORE() do { if (threadIdx.x == 0) for (int _i = 0; _i < 8; ++_i) g_phase_prof[blockIdx.x * 8 + _i] = _pacc[_i]; } while (0)
+#else
+#define PROF_INIT()
+#define PROF_MARK(i)
+#define PROF_STORE()
+#endif
+
 // ---------------------------------------------------------------- the fused polar kernel
 // MC: compile-time M (0 = runtime plan); when MC > 0 the ring FFT length is 2 MC.
 template <typename T, int W, int MC>
@@ -250,7 +295,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
   T2* twT = twM + M;
   T* dap = reinterpret_cast<T*>(twT + nt);
   T2* wscr = reinterpret_cast<T2*>(base + (((size_t)(M + nt) * sizeof(T2) + (size_t)L * sizeof(T) + 15) / 16) * 16);
-  const int MP = M + M / 16, NTP = nt + nt / 16;  // padded ping-pong lengths (padi)
+  const int MP = (M + 15) & ~15, NTP = (nt + 15) & ~15;   // ping-pong lengths: padi permutes within 16-blocks
   T2* region = wscr + (size_t)pp.fft_warps * 2 * MP;
   T2* myA = wscr + (size_t)warp * 2 * MP;         // row / column FFT ping-pong
   T2* myB = myA + MP;
@@ -260,8 +305,13 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
     const T2* gtM = reinterpret_cast<const T2*>(pp.tw_M);
     const T2* gtT = reinterpret_cast<const T2*>(pp.tw_theta);
     const T* gd = reinterpret_cast<const T*>(pp.deapod);
-    for (int i = tid; i < M; i += nthr) twM[i] = gtM[i];
-    for (int i = tid; i < nt; i += nthr) twT[i] = gtT[i];
+    if constexpr (MC > 0) {
+      build_stage_tw<T2, MC>(twM, gtM, tid, nthr);             // per-stage tables (<= M entries)
+      build_stage_tw<T2, NC>(twT, gtT, tid, nthr);
+    } else {
+      for (int i = tid; i < M; i += nthr) twM[i] = gtM[i];
+      for (int i = tid; i < nt; i += nthr) twT[i] = gtT[i];
+    }
     for (int i = tid; i < L; i += nthr) dap[i] = gd[i];
   }
   __syncthreads();
@@ -274,6 +324,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
   const Es<T> phi(pp.half_w, pp.beta);
   const int G = pp.ring_group;
 
+  PROF_INIT();
   for (int64_t img = blockIdx.x; img < n_img; img += gridDim.x) {
     const T* I = images + img * img_stride;
     // ---------------- K1a: row FFTs, two real rows per complex sequence, deapodised + zero-padded on load
@@ -308,6 +359,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       }
     }
     __syncthreads();
+    PROF_MARK(0);
 
     // ---------------- per phase: K1b column FFTs (input rows 0..L-1 = image rows, output fftshifted with
     // PADR wrapped duplicate rows), then K2 gather of node pairs (theta, pi - theta)
@@ -321,6 +373,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         for (int cc = lane; cc < ncols; cc += 32) dst[cc] = src[cc];
       }
       __syncthreads();
+      PROF_MARK(1);
       if (warp < pp.fft_warps) {
         for (int cc = warp; cc < ncols; cc += pp.fft_warps) {
           T2* col = Gc + cc;
@@ -338,6 +391,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         }
       }
       __syncthreads();
+      PROF_MARK(2);
       const int nb = pp.phase_node_begin[ph], ne = pp.phase_node_begin[ph + 1];
       for (int t = nb + tid; t < ne; t += nthr) {
         const uint32_t nd = __ldg(pp.nodes + t);
@@ -377,6 +431,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         if (pair) Pol[(int64_t)j * half + (half - l)] = accB;
       }
       __syncthreads();
+      PROF_MARK(3);
     }
 
     // ---------------- K3: ring FFTs (full ring rebuilt from the half ring), staged [k][jj], written k-major
@@ -398,31 +453,44 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         }
       }
       __syncthreads();
+      PROF_MARK(4);
       {
         // warp per k: lanes write rings j0 + lane (re row then im row), 128-B coalesced stores
         const int64_t kstride = n_img * 2 * (int64_t)n_xi;
-        T* dst = ghat + img * 2 * (int64_t)n_xi + j0 + (int64_t)warp * kstride;
-        const T2* sp = stg + (size_t)warp * GS;
-        for (int k = warp; k <= pp.k_max; k += nwarps) {
-          for (int jj = lane; jj < g; jj += 32) {
+        // g <= 16: each half-warp writes one k (two k per warp instruction); else a warp per k
+        const int per = g <= 16 ? 2 : 1;
+        const int sub = per == 2 ? (lane >> 4) : 0, ln = per == 2 ? (lane & 15) : lane, lstep = per == 2 ? 16 : 32;
+        const int k0 = warp * per + sub, kstep = nwarps * per;
+        T* dst = ghat + img * 2 * (int64_t)n_xi + j0 + (int64_t)k0 * kstride;
+        const T2* sp = stg + (size_t)k0 * GS;
+        for (int k = k0; k <= pp.k_max; k += kstep) {
+          for (int jj = ln; jj < g; jj += lstep) {
             const T2 v = sp[jj];
             dst[jj] = v.x;
             dst[jj + n_xi] = v.y;
           }
-          dst += nwarps * kstride;
-          sp += (size_t)nwarps * GS;
+          dst += kstep * kstride;
+          sp += (size_t)kstep * GS;
         }
       }
       __syncthreads();
+      PROF_MARK(5);
     }
   }
+  PROF_STORE();
 }
 
 int polar_max_smem() { return 227 * 1024; }
 
+#ifdef FBSPCA_PHASE_PROF
+extern "C" int fbspca_debug_phase_prof(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_phase_prof, sizeof(unsigned long long) * n);
+}
+#endif
+
 int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps) {
   return (int)(((sizeof(PolarParams) + 15) / 16) * 16) + (int)((((M + n_theta) * csz + L * (csz / 2)) + 15) / 16) * 16 +
-         nwarps * 2 * (M + M / 16) * csz;
+         nwarps * 2 * ((M + 15) & ~15) * csz;
 }
 
 template <typename T, int W, int MC>

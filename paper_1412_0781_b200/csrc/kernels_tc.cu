@@ -128,17 +128,19 @@ radial_tc_kernel(const float* __restrict__ ghat, const float* __restrict__ t_hi,
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(TC_M >> 4) << 24);
   const int nchunks = (n_xi + TC_KC - 1) / TC_KC;
 
-  for (int c = 0; c < nchunks; ++c) {
-    const int s = c & 1;
-    unsigned char* st = sm + s * stage_bytes;
-    if (c >= 2) mbar_wait(&bars[s], ((c - 2) >> 1) & 1);     // MMAs of chunk c-2 released this stage
-    const int j0 = c * TC_KC;
-    // A chunk: 128 rows x 32 fp32 -> hi / lo tiles
-    for (int idx = tid; idx < TC_M * 8; idx += 128) {
-      const int row = idx >> 3, c16 = idx & 7;
-      const int r = r0 + row, j = j0 + 4 * c16;
+  // A chunk: 128 rows x 32 fp32 -> hi / lo tiles.  Item idx = tid + 128 u (u < 8): a warp covers 8
+  // consecutive rows x 4 sixteen-byte chunks, so each 8-lane group stores one contiguous 128-B core-matrix
+  // row block (conflict-free) and each row is read as a 64-B run.  Chunk c+1 is loaded into registers
+  // before chunk c is split and stored (two chunks of loads in flight per thread).
+  auto load_a = [&](int cc, float4* dst) {
+    const int jb = cc * TC_KC;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = tid + 128 * u, w = idx >> 5, ln = idx & 31;
+      const int row = (w & 15) * 8 + (ln & 7), c16 = (w >> 4) * 4 + (ln >> 3);
+      const int r = r0 + row, j = jb + 4 * c16;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r < rows) {
+      if (r < rows && cc < nchunks) {
         const float* src = A + (int64_t)r * n_xi + j;
         if (j + 3 < n_xi) v = __ldg(reinterpret_cast<const float4*>(src));
         else {
@@ -147,15 +149,32 @@ radial_tc_kernel(const float* __restrict__ ghat, const float* __restrict__ t_hi,
           if (j + 2 < n_xi) v.z = src[2];
         }
       }
-      float4 h = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
-      float4 lo = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+      dst[u] = v;
+    }
+  };
+  float4 va[8], vn[8];
+  load_a(0, va);
+  for (int c = 0; c < nchunks; ++c) {
+    const int s = c & 1;
+    unsigned char* st = sm + s * stage_bytes;
+    const int j0 = c * TC_KC;
+    load_a(c + 1, vn);                                        // prefetch the next chunk
+    if (c >= 2) mbar_wait(&bars[s], ((c - 2) >> 1) & 1);     // MMAs of chunk c-2 released this stage
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = tid + 128 * u, w = idx >> 5, ln = idx & 31;
+      const int row = (w & 15) * 8 + (ln & 7), c16 = (w >> 4) * 4 + (ln >> 3);
+      const float4 v = va[u];
+      const float4 h = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+      const float4 lo = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
       const uint32_t off = il_off(row, c16, TC_M);
       *reinterpret_cast<float4*>(st + off) = h;
       *reinterpret_cast<float4*>(st + a_bytes + off) = lo;
     }
     // B chunk: N rows (q) x 32 (pre-split on the host)
     for (int idx = tid; idx < N * 8; idx += 128) {
-      const int q = idx >> 3, c16 = idx & 7;
+      const int w = idx >> 5, ln = idx & 31;         // same conflict-free mapping: 8 rows x 4 chunks per warp
+      const int q = ((w >> 1) * 8) + (ln & 7), c16 = (w & 1) * 4 + (ln >> 3);
       const int j = j0 + 4 * c16;
       float4 h = make_float4(0.f, 0.f, 0.f, 0.f), lo = h;
       if (q < pk) {
@@ -196,6 +215,8 @@ radial_tc_kernel(const float* __restrict__ ghat, const float* __restrict__ t_hi,
       }
       __syncwarp();
     }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) va[u] = vn[u];
   }
   // the last commit tracks every MMA issued before it
   mbar_wait(&bars[(nchunks - 1) & 1], ((nchunks - 1) >> 1) & 1);
@@ -243,6 +264,144 @@ cudaError_t launch_radial_tc(const Plan& P, int64_t nb, int64_t i0, int64_t ld, 
   dim3 grid((unsigned)((2 * nb + TC_M - 1) / TC_M), (unsigned)(P.k_max + 1));
   radial_tc_kernel<<<grid, 128, smem, s>>>((const float*)P.d_ghat, P.d_table_hi, P.d_table_lo,
                                           P.d_p, P.d_coef_off, (int)nb, P.n_xi, i0, ld, cols, (float*)d_coeffs);
+  return cudaGetLastError();
+}
+
+}  // namespace fbspca
+
+// ---------------------------------------------------------------- K5 on tcgen05 (Eqs. (ck), (ck_0))
+// CTA (k, chunk): S = A A^T over the chunk's kCovChunk images (2 kCovChunk real columns, re/im interleaved),
+// A = block k (p_k rows x columns, K-major).  Both MMA operands come from the same shared tile (rows padded
+// to R = roundup16(p_k) <= 256; M = 128 per tile, two M-tiles when R > 128).  3xTF32 products accumulate in
+// fp32 in TMEM over the chunk; the upper triangle is stored as fp64 into scratch[chunk] (the fixed-order
+// reduction over chunks is cov_reduce_kernel).  k = 0 also accumulates s_0 = sum_i a_{0,i} in fp64.
+namespace fbspca {
+
+__global__ void __launch_bounds__(128, 1)
+cov_tc_kernel(const float* __restrict__ coeffs, const int* __restrict__ p, const int64_t* __restrict__ coef_off,
+              const int64_t* __restrict__ blk_off, int64_t ld, int64_t i0, int64_t nb, int k_max, int tmem_cols,
+              int tile_rows, double* __restrict__ scratch, int64_t scratch_stride) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  const int k = blockIdx.x + 1;                                  // k = 0 runs on the fp64 SIMT path (F9)
+  const int pk = p[k];
+  const int R = (pk + 15) & ~15;
+  const int nmt = R > 128 ? 2 : 1;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t img0 = i0 + (int64_t)blockIdx.y * kCovChunk;
+  const int64_t cnb = min((int64_t)kCovChunk, i0 + nb - img0);
+  const int ncols = int(2 * cnb);
+  const uint32_t tile_bytes = uint32_t(tile_rows) * TC_KC * 4;  // sized for the largest R of k >= 1
+  const uint32_t stage_bytes = 2 * tile_bytes;                   // hi + lo
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 2 * stage_bytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) { mbar_init(&bars[0], 1); mbar_init(&bars[1], 1); }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem_d = *tmem_slot;
+  const float* A = coeffs + coef_off[k] * 2 * ld + 2 * img0;
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(R >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+  const int nchunks = (ncols + TC_KC - 1) / TC_KC;
+  const uint32_t lbo = uint32_t(tile_rows / 8) * 128;           // tile laid out with tile_rows >= 128 rows
+
+  for (int c = 0; c < nchunks; ++c) {
+    const int s = c & 1;
+    unsigned char* st = sm + s * stage_bytes;
+    if (c >= 2) mbar_wait(&bars[s], ((c - 2) >> 1) & 1);
+    const int j0 = c * TC_KC;
+    const int items = R * 8;
+    for (int idx = tid; idx < items; idx += 128) {
+      const int w = idx >> 5, ln = idx & 31;
+      const int row = (w >> 1) * 8 + (ln & 7), c16 = (w & 1) * 4 + (ln >> 3);
+      const int j = j0 + 4 * c16;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (row < pk) {
+        const float* src = A + (int64_t)row * 2 * ld + j;
+        if (j + 3 < ncols) v = __ldg(reinterpret_cast<const float4*>(src));
+        else {
+          if (j < ncols) v.x = src[0];
+          if (j + 1 < ncols) v.y = src[1];
+          if (j + 2 < ncols) v.z = src[2];
+        }
+      }
+      const float4 h = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+      const float4 lo = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+      const uint32_t off = il_off(row, c16, tile_rows);
+      *reinterpret_cast<float4*>(st + off) = h;
+      *reinterpret_cast<float4*>(st + tile_bytes + off) = lo;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (lane == 0) {
+        const uint32_t base = smem_u32(st);
+#pragma unroll
+        for (int s4 = 0; s4 < TC_KC / 8; ++s4) {
+          const uint32_t ko = uint32_t(2 * s4) * lbo;
+          const uint64_t bh = make_desc(base + ko, lbo, 128);
+          const uint64_t bl = make_desc(base + tile_bytes + ko, lbo, 128);
+          for (int mt = 0; mt < nmt; ++mt) {
+            const uint32_t mo = uint32_t(mt) * 16u * 128u;          // 128 rows further
+            const uint64_t ah = make_desc(base + ko + mo, lbo, 128);
+            const uint64_t al = make_desc(base + tile_bytes + ko + mo, lbo, 128);
+            const uint32_t d = tmem_d + uint32_t(mt * 256);
+            mma_tf32(d, ah, bh, idesc, (c | s4) ? 1u : 0u);
+            mma_tf32(d, ah, bl, idesc, 1u);
+            mma_tf32(d, al, bh, idesc, 1u);
+          }
+        }
+        mma_commit(&bars[s]);
+      }
+      __syncwarp();
+    }
+  }
+  mbar_wait(&bars[(nchunks - 1) & 1], ((nchunks - 1) >> 1) & 1);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  double* dst = scratch + (int64_t)blockIdx.y * scratch_stride + blk_off[k];
+  for (int mt = 0; mt < nmt; ++mt) {
+    const int q = mt * 128 + 32 * warp + lane;
+    for (int q0 = 0; q0 < R; q0 += 16) {
+      float v[16];
+      tmem_ld16(tmem_d + uint32_t(mt * 256) + (uint32_t(32 * warp) << 16) + uint32_t(q0), v);
+      if (q < pk) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int qq = q0 + i;
+          if (qq >= q && qq < pk) dst[(int64_t)q * pk - (int64_t)q * (q - 1) / 2 + (qq - q)] = double(v[i]);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(tmem_cols));
+}
+
+cudaError_t launch_cov_tc(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb, cudaStream_t s) {
+  if (P.k_max < 1) return cudaSuccess;
+  const int R = (P.p[1] + 15) & ~15;                  // largest p_k over k >= 1
+  if (R > 256) return cudaErrorInvalidValue;
+  const int cols = R > 128 ? 512 : radial_tc_cols(P.p[1]);
+  const int TR = R > 128 ? 256 : 128;                  // the M = 128 A operand reads 128 rows
+  const int smem = 2 * (2 * TR * TC_KC * 4) + 64;
+  static int configured = 0;
+  if (configured < smem) {
+    cudaError_t e = cudaFuncSetAttribute(cov_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  const int nchunk = (int)((nb + kCovChunk - 1) / kCovChunk);
+  const int64_t total = P.blk_off[P.k_max + 1] + P.p[0] + 1;
+  dim3 grid((unsigned)P.k_max, (unsigned)nchunk);
+  cov_tc_kernel<<<grid, 128, smem, s>>>((const float*)d_coeffs, P.d_p, P.d_coef_off, P.d_blk_off, ld, i0, nb, P.k_max,
+                                        cols, TR, P.d_cov_scratch, total);
   return cudaGetLastError();
 }
 

@@ -215,9 +215,15 @@ fbspca_status build_host_plan(Plan& P) {
   const int fixed = polar_fixed_smem(M, P.n_theta, L, csz, pp.fft_warps);
   const int budget = cap - fixed;
   const int kk = (P.k_max + 1) | 1;                    // staging row stride (odd)
-  const int ntp = P.n_theta + P.n_theta / 16;          // padded ping-pong length
-  pp.ang_warps = std::min(8, (budget - 32 * kk * csz) / (2 * ntp * csz));
-  if (pp.ang_warps < 1) pp.ang_warps = std::min(8, (budget - kk * csz) / (2 * ntp * csz));
+  const int ntp = (P.n_theta + 15) & ~15;               // ping-pong length (swizzle permutes 16-blocks)
+  // angular pass: (warps running ring FFTs, rings staged per group); prefer all 16 warps busy
+  const int cand[][2] = {{16, 16}, {8, 32}, {8, 16}, {4, 16}, {4, 8}, {2, 8}, {1, 4}, {1, 1}};
+  pp.ang_warps = 0;
+  int Gsel = 1;
+  for (auto& c : cand) {
+    const int g = std::min(c[1], P.n_xi);
+    if (c[0] * 2 * ntp * csz + (g | 1) * kk * csz <= budget) { pp.ang_warps = c[0]; Gsel = g; break; }
+  }
   if (pp.ang_warps < 1 || budget < M * 11 * csz) {
     set_error("image too large for the fused polar kernel's shared memory"); return FBSPCA_ERR_CONFIG;
   }
@@ -227,8 +233,7 @@ fbspca_status build_host_plan(Plan& P) {
   if (S % 2 == 0) --S;                                   // odd row stride (bank spread)
   if (S > pp.ncols_x) S = pp.ncols_x | 1;
   pp.S = S;
-  int G = (budget - ang_scr) / ((kk + 1) * csz) - 1;
-  G = std::max(1, std::min(G, std::min(32, P.n_xi)));
+  const int G = Gsel;
   pp.ring_group = G;
   const int region = std::max(std::max(rows_g * S * csz, pp.fft_warps * M * csz), ang_scr + (G | 1) * kk * csz);
   pp.smem_region_bytes = region;
@@ -251,7 +256,17 @@ fbspca_status build_host_plan(Plan& P) {
       // pair leaders only: node (j, half - l) = (-k1, k2) is gathered with (j, l) (same columns)
       if (2 * l <= half) ph.push_back((uint32_t(j) << 16) | uint32_t(l));
     }
-    std::sort(ph.begin(), ph.end());                      // ring-major within a phase
+    // order by (b1, b2): a warp's lanes then read the same grid rows at neighbouring columns, which keeps
+    // the gather's shared-memory accesses close to conflict-free (ring-major order: ~2x wavefronts)
+    std::sort(ph.begin(), ph.end(), [&](uint32_t x, uint32_t y) {
+      auto key = [&](uint32_t nd) {
+        const int j = int(nd >> 16), l = int(nd & 0xffffu);
+        const double k1 = rho[j] * cs[2 * l], k2 = rho[j] * cs[2 * l + 1];
+        return std::make_pair(int(std::ceil(k1 - hw)), int(std::ceil(k2 - hw)));
+      };
+      auto kx = key(x), ky = key(y);
+      return kx != ky ? kx < ky : x < y;
+    });
     P.nodes.insert(P.nodes.end(), ph.begin(), ph.end());
     ++np;
     lo = lo + S - w + 1;
