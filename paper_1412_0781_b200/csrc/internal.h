@@ -47,6 +47,7 @@ struct PolarParams {
   const double* rho;              // n_xi: xi_j * M
   const double* cs;               // half x 2: cos(theta_l), sin(theta_l)
   const uint32_t* nodes;          // (j << 16) | l, grouped by phase
+  const int4* noderec;            // per entry {b1 | b2 << 16, t1, t2, (j << 16) | l} (fp32 path)
   void* xscratch;                 // per resident CTA: L x ncols_x complex
   void* pscratch;                 // per resident CTA: n_xi x half complex
   int64_t xscratch_stride, pscratch_stride;   // complex elements per CTA
@@ -78,6 +79,7 @@ struct Plan {
   std::vector<double> rho, cs;           // xi_j M; (cos, sin)(theta_l), l < n_theta/2
   PolarParams pp{};                      // host copy (device pointers filled at upload)
   std::vector<uint32_t> nodes;
+  std::vector<int32_t> noderec;          // 4 per node entry
   int polar_smem = 0;
   int polar_grid = 0;                    // resident CTAs of the polar kernel
   // device buffers
@@ -91,6 +93,7 @@ struct Plan {
   double* d_rho = nullptr;
   double* d_cs = nullptr;
   uint32_t* d_nodes = nullptr;
+  int32_t* d_noderec = nullptr;
   PolarParams* d_pp = nullptr;           // device copy of pp
   void* d_xscratch = nullptr;
   void* d_pscratch = nullptr;

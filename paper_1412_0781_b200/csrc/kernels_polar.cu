@@ -123,6 +123,9 @@ __device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tws,
 // (unswizzled: 2.1x).
 __device__ __forceinline__ int padi(int i) { return i ^ ((3 * (i >> 4)) & 15); }
 
+// which ping-pong buffer the last stage of fft_pow2<N> does NOT read (so the result may be stored there)
+template <int N> __host__ __device__ constexpr bool fft_result_in_A() { return N == 128 || N == 256 || N == 512; }
+
 // stage list per size: (R, Ns) ... ; table offsets TOFF accumulate (R - 1) Ns over stages with Ns > 1
 template <typename T2, int R, int Ns>
 __device__ __forceinline__ void fill_stage_tw(T2* dst, const T2* __restrict__ lin, int N, int tid, int nthr) {
@@ -341,19 +344,31 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           const T db = dap[b];
           return T2{__ldg(r0 + b) * d0 * db, __ldg(r1 + b) * d1 * db};
         };
-        T2* res = region + (size_t)warp * M;                         // the phase region is free here
-        auto st = [res](int i, T2 v) { res[i] = v; };
+        // pow2: the result stays in the warp's (swizzled) ping-pong buffer and phase-0 columns go straight
+        // into the shared grid (rows = image rows); only columns of later phases go through X.
+        // runtime sizes: the result goes to a per-warp slice of the (still free) phase region.
+        T2* res = (MC > 0) ? (fft_result_in_A<MC>() ? myA : myB) : region + (size_t)warp * M;
+        auto st = [res](int i, T2 v) { res[MC > 0 ? padi(i) : i] = v; };
         fft_any<T2, MC>(pp.fft_M, ld, st, myA, myB, twM, lane);
+        const int lo0 = pp.phase_lo[0], hi0 = lo0 + (S < col_lo + ncx - lo0 ? S : col_lo + ncx - lo0);
+        const int lo1 = pp.n_phase > 1 ? pp.phase_lo[1] : (1 << 30);
         for (int cc = lane; cc < ncx; cc += 32) {
           int m = (col_lo + cc) % M; if (m < 0) m += M;
           int mm = M - m; if (mm == M) mm = 0;
-          T2 zm = res[m], zc = res[mm];
+          T2 zm = res[MC > 0 ? padi(m) : m], zc = res[MC > 0 ? padi(mm) : mm];
           zc.y = -zc.y;                                              // conj Z(-m)
           const T2 xa = {T(0.5) * (zm.x + zc.x), T(0.5) * (zm.y + zc.y)};
           const T2 dd = csub(zm, zc);
           const T2 xb = {T(0.5) * dd.y, T(-0.5) * dd.x};             // (Z(m) - conj Z(-m)) / (2i)
-          X[(int64_t)a0 * ncx + cc] = xa;
-          if (has1) X[(int64_t)a1 * ncx + cc] = xb;
+          const int m2 = col_lo + cc;
+          if (MC == 0 || m2 >= lo1) {
+            X[(int64_t)a0 * ncx + cc] = xa;
+            if (has1) X[(int64_t)a1 * ncx + cc] = xb;
+          }
+          if (MC > 0 && m2 < hi0) {
+            region[(size_t)a0 * S + (m2 - lo0)] = xa;
+            if (has1) region[(size_t)a1 * S + (m2 - lo0)] = xb;
+          }
         }
         __syncwarp();
       }
@@ -367,12 +382,14 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       const int lo = pp.phase_lo[ph];
       int ncols = col_lo + ncx - lo; if (ncols > S) ncols = S;
       T2* Gc = region;
-      for (int a = warp; a < L; a += nwarps) {
-        const T2* src = X + (int64_t)a * ncx + (lo - col_lo);
-        T2* dst = Gc + (size_t)a * S;
-        for (int cc = lane; cc < ncols; cc += 32) dst[cc] = src[cc];
+      if (MC == 0 || ph > 0) {                      // pow2 phase 0 was written by the row pass directly
+        for (int a = warp; a < L; a += nwarps) {
+          const T2* src = X + (int64_t)a * ncx + (lo - col_lo);
+          T2* dst = Gc + (size_t)a * S;
+          for (int cc = lane; cc < ncols; cc += 32) dst[cc] = src[cc];
+        }
+        __syncthreads();
       }
-      __syncthreads();
       PROF_MARK(1);
       if (warp < pp.fft_warps) {
         for (int cc = warp; cc < ncols; cc += pp.fft_warps) {
@@ -394,14 +411,23 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       PROF_MARK(2);
       const int nb = pp.phase_node_begin[ph], ne = pp.phase_node_begin[ph + 1];
       for (int t = nb + tid; t < ne; t += nthr) {
-        const uint32_t nd = __ldg(pp.nodes + t);
-        const int j = int(nd >> 16), l = int(nd & 0xffffu);
+        int j, l, b1, b2;
+        T t1, t2;
+        if constexpr (sizeof(T) == 4) {             // fp32: precomputed record (one 16-B load)
+          const int4 rec = __ldg(pp.noderec + t);
+          b1 = int(short(rec.x & 0xFFFF)); b2 = rec.x >> 16;
+          t1 = __int_as_float(rec.y); t2 = __int_as_float(rec.z);
+          j = int(uint32_t(rec.w) >> 16); l = rec.w & 0xFFFF;
+        } else {                                    // fp64: node coordinates in fp64 on the fly
+          const uint32_t nd = __ldg(pp.nodes + t);
+          j = int(nd >> 16); l = int(nd & 0xffffu);
+          const double r = __ldg(pp.rho + j);
+          const double k1 = r * __ldg(pp.cs + 2 * l), k2 = r * __ldg(pp.cs + 2 * l + 1);
+          const double f1 = ceil(k1 - pp.half_w), f2 = ceil(k2 - pp.half_w);
+          b1 = int(f1); b2 = int(f2);
+          t1 = T(k1 - f1); t2 = T(k2 - f2);
+        }
         const bool pair = (l != 0) && (2 * l != half);
-        const double r = __ldg(pp.rho + j);
-        const double k1 = r * __ldg(pp.cs + 2 * l), k2 = r * __ldg(pp.cs + 2 * l + 1);
-        const double f1 = ceil(k1 - pp.half_w), f2 = ceil(k2 - pp.half_w);
-        const int b1 = int(f1), b2 = int(f2);
-        const T t1 = T(k1 - f1), t2 = T(k2 - f2);
         T wx[W], wy[W];
 #pragma unroll
         for (int q = 0; q < W; ++q) { wx[q] = phi(t1 - T(q)); wy[q] = phi(t2 - T(q)); }

@@ -256,18 +256,33 @@ fbspca_status build_host_plan(Plan& P) {
       // pair leaders only: node (j, half - l) = (-k1, k2) is gathered with (j, l) (same columns)
       if (2 * l <= half) ph.push_back((uint32_t(j) << 16) | uint32_t(l));
     }
-    // order by (b1, b2): a warp's lanes then read the same grid rows at neighbouring columns, which keeps
-    // the gather's shared-memory accesses close to conflict-free (ring-major order: ~2x wavefronts)
+    // Order for the gather's shared-memory accesses (64-bit loads resolve per half-warp, 16 bank slots):
+    // group entries by row anchor b1 so lanes read the same grid rows, and within a row deal them
+    // round-robin over b2 mod 16 so the 16 lanes of a half-warp hit distinct slots (equal anchors
+    // broadcast).  (ring-major order: ~2x ideal wavefronts; plain (b1, b2) order: ~1.5x.)
+    auto key = [&](uint32_t nd) {
+      const int j = int(nd >> 16), l = int(nd & 0xffffu);
+      const double k1 = rho[j] * cs[2 * l], k2 = rho[j] * cs[2 * l + 1];
+      return std::make_pair(int(std::ceil(k1 - hw)), int(std::ceil(k2 - hw)));
+    };
     std::sort(ph.begin(), ph.end(), [&](uint32_t x, uint32_t y) {
-      auto key = [&](uint32_t nd) {
-        const int j = int(nd >> 16), l = int(nd & 0xffffu);
-        const double k1 = rho[j] * cs[2 * l], k2 = rho[j] * cs[2 * l + 1];
-        return std::make_pair(int(std::ceil(k1 - hw)), int(std::ceil(k2 - hw)));
-      };
       auto kx = key(x), ky = key(y);
       return kx != ky ? kx < ky : x < y;
     });
-    P.nodes.insert(P.nodes.end(), ph.begin(), ph.end());
+    std::vector<uint32_t> dealt;
+    dealt.reserve(ph.size());
+    for (size_t a = 0; a < ph.size();) {
+      size_t b = a;
+      const int row = key(ph[a]).first;
+      while (b < ph.size() && key(ph[b]).first == row) ++b;
+      std::vector<std::vector<uint32_t>> bucket(16);
+      for (size_t e = a; e < b; ++e) bucket[((key(ph[e]).second % 16) + 16) % 16].push_back(ph[e]);
+      for (size_t round = 0, left = b - a; left > 0; ++round)
+        for (int r = 0; r < 16; ++r)
+          if (round < bucket[r].size()) { dealt.push_back(bucket[r][round]); --left; }
+      a = b;
+    }
+    P.nodes.insert(P.nodes.end(), dealt.begin(), dealt.end());
     ++np;
     lo = lo + S - w + 1;
   }
@@ -275,6 +290,23 @@ fbspca_status build_host_plan(Plan& P) {
   pp.phase_node_begin[np] = int(P.nodes.size());
   P.rho = rho;
   P.cs = cs;
+  // per-entry record for the fp32 gather: {b1 | b2 << 16, t1, t2, (j << 16) | l}, the same fp64 arithmetic
+  // the fp64 kernel path performs on the fly (k = rho_j (cos, sin) theta_l, b = ceil(k - w/2), t = k - b)
+  P.noderec.resize(4 * P.nodes.size());
+  for (size_t e = 0; e < P.nodes.size(); ++e) {
+    const uint32_t nd = P.nodes[e];
+    const int j = int(nd >> 16), l = int(nd & 0xffffu);
+    const double k1 = rho[j] * cs[2 * l], k2 = rho[j] * cs[2 * l + 1];
+    const double f1 = std::ceil(k1 - hw), f2 = std::ceil(k2 - hw);
+    const float t1 = float(k1 - f1), t2 = float(k2 - f2);
+    const int b1 = int(f1), b2 = int(f2);
+    int32_t rec[4];
+    rec[0] = int32_t((uint32_t(b1) & 0xFFFFu) | (uint32_t(b2) << 16));
+    std::memcpy(&rec[1], &t1, 4);
+    std::memcpy(&rec[2], &t2, 4);
+    rec[3] = int32_t(nd);
+    std::memcpy(&P.noderec[4 * e], rec, 16);
+  }
   return FBSPCA_OK;
 }
 
