@@ -21,6 +21,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+BATCH = 4096          # images per expand batch (ghat workspace); see DESIGN.md "Measurement"
 METRIC = "images/sec (expansion+covariance, L=128) at 1/2/4/8 B200; % HBM roofline"
 
 
@@ -33,6 +34,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=0, help="override total images (testing only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--batch", type=int, default=BATCH, help="images per expand batch (plan max_batch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -189,7 +191,8 @@ def main():
     s, e = F.shard_range(n, rank, world)
     n_local = e - s
     dt = F.F32 if cfg["dtype"] == "f32" else F.F64
-    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], dtype=dt, device=local, max_batch=4096)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], dtype=dt, device=local, max_batch=args.batch)
+    plan.bench_batch = args.batch
     comm = None
     if world > 1:
         uid = torch.zeros(128, dtype=torch.uint8)
@@ -363,7 +366,7 @@ def main():
 
 
 def plan_batch(plan):
-    return 4096
+    return getattr(plan, "bench_batch", BATCH)
 
 
 if __name__ == "__main__":

@@ -330,19 +330,34 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
   PROF_INIT();
   for (int64_t img = blockIdx.x; img < n_img; img += gridDim.x) {
     const T* I = images + img * img_stride;
+    // ---------------- stage the image in shared memory (all threads, 16-byte loads when possible)
+    const T* Isrc = I;
+    if (pp.img_off >= 0) {
+      T* simg = reinterpret_cast<T*>(region + pp.img_off);
+      const int nel = L * L;
+      if ((nel * (int)sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(I) & 15) == 0) {
+        const int4* src = reinterpret_cast<const int4*>(I);
+        int4* dst = reinterpret_cast<int4*>(simg);
+        for (int i = tid; i < nel * (int)sizeof(T) / 16; i += nthr) dst[i] = __ldg(src + i);
+      } else {
+        for (int i = tid; i < nel; i += nthr) simg[i] = __ldg(I + i);
+      }
+      __syncthreads();
+      Isrc = simg;
+    }
     // ---------------- K1a: row FFTs, two real rows per complex sequence, deapodised + zero-padded on load
     if (warp < pp.fft_warps) {
       for (int pr = warp; pr < (L + 1) / 2; pr += pp.fft_warps) {
         const int a0 = 2 * pr, a1 = a0 + 1;
         const bool has1 = a1 < L;
-        const T* r0 = I + (int64_t)a0 * L;
-        const T* r1 = I + (int64_t)(has1 ? a1 : a0) * L;
+        const T* r0 = Isrc + (int64_t)a0 * L;
+        const T* r1 = Isrc + (int64_t)(has1 ? a1 : a0) * L;
         const T d0 = dap[a0], d1 = has1 ? dap[a1] : T(0);
         auto ld = [&](int t) -> T2 {
           const int b = (t < M / 2 ? t : t - M) + L / 2;          // pixel column of FFT position t
           if (b < 0 || b >= L) return T2{T(0), T(0)};
           const T db = dap[b];
-          return T2{__ldg(r0 + b) * d0 * db, __ldg(r1 + b) * d1 * db};
+          return T2{r0[b] * d0 * db, r1[b] * d1 * db};
         };
         // pow2: the result stays in the warp's (swizzled) ping-pong buffer and phase-0 columns go straight
         // into the shared grid (rows = image rows); only columns of later phases go through X.

@@ -237,6 +237,11 @@ fbspca_status build_host_plan(Plan& P) {
   pp.ring_group = G;
   const int region = std::max(std::max(rows_g * S * csz, pp.fft_warps * M * csz), ang_scr + (G | 1) * kk * csz);
   pp.smem_region_bytes = region;
+  {   // image staged behind the phase-0 grid rows (pow2) or the per-warp row results (runtime sizes)
+    const int used = std::max(L * S, pp.fft_warps * M);            // complex elements
+    const int need = used + (L * L * (csz / 2) + csz - 1) / csz + 2;
+    pp.img_off = (need * csz <= region) ? ((used + 1) & ~1) : -1;    // 16-B aligned start
+  }
   P.polar_smem = fixed + region;
   // phases over columns: phase p holds m2 in [lo_p, lo_p + S) and owns nodes with b2 in [lo_p, lo_p + S - w]
   std::vector<int> order(b2.size());
@@ -256,10 +261,9 @@ fbspca_status build_host_plan(Plan& P) {
       // pair leaders only: node (j, half - l) = (-k1, k2) is gathered with (j, l) (same columns)
       if (2 * l <= half) ph.push_back((uint32_t(j) << 16) | uint32_t(l));
     }
-    // Order for the gather's shared-memory accesses (64-bit loads resolve per half-warp, 16 bank slots):
-    // group entries by row anchor b1 so lanes read the same grid rows, and within a row deal them
-    // round-robin over b2 mod 16 so the 16 lanes of a half-warp hit distinct slots (equal anchors
-    // broadcast).  (ring-major order: ~2x ideal wavefronts; plain (b1, b2) order: ~1.5x.)
+    // Order for the gather's shared-memory accesses: by row anchor b1, then column anchor b2, so a warp's
+    // lanes read the same grid rows at neighbouring columns (ring-major order: ~2x ideal wavefronts;
+    // (b1, b2) order: ~1.5x).
     auto key = [&](uint32_t nd) {
       const int j = int(nd >> 16), l = int(nd & 0xffffu);
       const double k1 = rho[j] * cs[2 * l], k2 = rho[j] * cs[2 * l + 1];
@@ -269,20 +273,9 @@ fbspca_status build_host_plan(Plan& P) {
       auto kx = key(x), ky = key(y);
       return kx != ky ? kx < ky : x < y;
     });
-    std::vector<uint32_t> dealt;
-    dealt.reserve(ph.size());
-    for (size_t a = 0; a < ph.size();) {
-      size_t b = a;
-      const int row = key(ph[a]).first;
-      while (b < ph.size() && key(ph[b]).first == row) ++b;
-      std::vector<std::vector<uint32_t>> bucket(16);
-      for (size_t e = a; e < b; ++e) bucket[((key(ph[e]).second % 16) + 16) % 16].push_back(ph[e]);
-      for (size_t round = 0, left = b - a; left > 0; ++round)
-        for (int r = 0; r < 16; ++r)
-          if (round < bucket[r].size()) { dealt.push_back(bucket[r][round]); --left; }
-      a = b;
-    }
-    P.nodes.insert(P.nodes.end(), dealt.begin(), dealt.end());
+    // (Measured: dealing a row's entries round-robin over b2 mod 16 removes slot collisions but is slower
+    // on B200 -- 145k vs 122k cycles/image for the C3 gather -- so the plain (b1, b2) order is kept.)
+    P.nodes.insert(P.nodes.end(), ph.begin(), ph.end());
     ++np;
     lo = lo + S - w + 1;
   }
