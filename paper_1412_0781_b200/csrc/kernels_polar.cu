@@ -504,14 +504,27 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         const int k0 = warp * per + sub, kstep = nwarps * per;
         T* dst = ghat + img * 2 * (int64_t)n_xi + j0 + (int64_t)k0 * kstride;
         const T2* sp = stg + (size_t)k0 * GS;
-        for (int k = k0; k <= pp.k_max; k += kstep) {
-          for (int jj = ln; jj < g; jj += lstep) {
-            const T2 v = sp[jj];
-            dst[jj] = v.x;
-            dst[jj + n_xi] = v.y;
+        const int kmx = pp.k_max;
+        (void)lstep;                                  // g <= G <= 32: one element per lane and k
+        const bool act = ln < g;
+        // 4 k per iteration: all shared loads first, then the global stores (independent -> ILP)
+        for (int k = k0; k <= kmx; k += 4 * kstep) {
+          T2 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const bool ok = act && (k + u * kstep <= kmx);
+            v[u] = ok ? sp[(size_t)u * kstep * GS + ln] : T2{T(0), T(0)};
           }
-          dst += kstep * kstride;
-          sp += (size_t)kstep * GS;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (act && (k + u * kstep <= kmx)) {
+              T* d = dst + (int64_t)u * kstep * kstride;
+              d[ln] = v[u].x;
+              d[ln + n_xi] = v[u].y;
+            }
+          }
+          dst += 4 * (int64_t)kstep * kstride;
+          sp += (size_t)4 * kstep * GS;
         }
       }
       __syncthreads();

@@ -23,7 +23,8 @@ namespace fbspca {
 namespace {
 
 constexpr int TC_M = 128;     // rows per CTA (64 images x re/im)
-constexpr int TC_KC = 32;     // K elements per pipeline chunk (4 MMAs of K = 8)
+constexpr int TC_KC = 32;     // K elements per pipeline chunk of the covariance kernel (4 MMAs of K = 8)
+constexpr int RK_KC = 16;     // K elements per pipeline chunk of the radial kernel (2 MMAs; 48 KB smem -> 4 CTAs/SM)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -106,7 +107,7 @@ radial_tc_kernel(const float* __restrict__ ghat, const float* __restrict__ t_hi,
   const int r0 = blockIdx.x * TC_M;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NMAX = tmem_cols;                    // B tiles sized for the largest N of the plan
-  const uint32_t a_bytes = TC_M * TC_KC * 4, b_bytes = uint32_t(NMAX) * TC_KC * 4;
+  const uint32_t a_bytes = TC_M * RK_KC * 4, b_bytes = uint32_t(NMAX) * RK_KC * 4;
   const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 2 * stage_bytes);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
@@ -126,18 +127,18 @@ radial_tc_kernel(const float* __restrict__ ghat, const float* __restrict__ t_hi,
   const float* Bh = t_hi + coef_off[k] * n_xi;
   const float* Bl = t_lo + coef_off[k] * n_xi;
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(TC_M >> 4) << 24);
-  const int nchunks = (n_xi + TC_KC - 1) / TC_KC;
+  const int nchunks = (n_xi + RK_KC - 1) / RK_KC;
 
-  // A chunk: 128 rows x 32 fp32 -> hi / lo tiles.  Item idx = tid + 128 u (u < 8): a warp covers 8
+  // A chunk: 128 rows x 16 fp32 -> hi / lo tiles.  Item idx = tid + 128 u (u < 4): a warp covers 8
   // consecutive rows x 4 sixteen-byte chunks, so each 8-lane group stores one contiguous 128-B core-matrix
-  // row block (conflict-free) and each row is read as a 64-B run.  Chunk c+1 is loaded into registers
+  // row block (conflict-free) and each row is read as one 64-B run.  Chunk c+1 is loaded into registers
   // before chunk c is split and stored (two chunks of loads in flight per thread).
   auto load_a = [&](int cc, float4* dst) {
-    const int jb = cc * TC_KC;
+    const int jb = cc * RK_KC;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 4; ++u) {
       const int idx = tid + 128 * u, w = idx >> 5, ln = idx & 31;
-      const int row = (w & 15) * 8 + (ln & 7), c16 = (w >> 4) * 4 + (ln >> 3);
+      const int row = w * 8 + (ln & 7), c16 = ln >> 3;
       const int r = r0 + row, j = jb + 4 * c16;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (r < rows && cc < nchunks) {
@@ -152,18 +153,18 @@ radial_tc_kernel(const float* __restrict__ ghat, const float* __restrict__ t_hi,
       dst[u] = v;
     }
   };
-  float4 va[8], vn[8];
+  float4 va[4], vn[4];
   load_a(0, va);
   for (int c = 0; c < nchunks; ++c) {
     const int s = c & 1;
     unsigned char* st = sm + s * stage_bytes;
-    const int j0 = c * TC_KC;
+    const int j0 = c * RK_KC;
     load_a(c + 1, vn);                                        // prefetch the next chunk
     if (c >= 2) mbar_wait(&bars[s], ((c - 2) >> 1) & 1);     // MMAs of chunk c-2 released this stage
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 4; ++u) {
       const int idx = tid + 128 * u, w = idx >> 5, ln = idx & 31;
-      const int row = (w & 15) * 8 + (ln & 7), c16 = (w >> 4) * 4 + (ln >> 3);
+      const int row = w * 8 + (ln & 7), c16 = ln >> 3;
       const float4 v = va[u];
       const float4 h = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
       const float4 lo = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
@@ -171,10 +172,10 @@ radial_tc_kernel(const float* __restrict__ ghat, const float* __restrict__ t_hi,
       *reinterpret_cast<float4*>(st + off) = h;
       *reinterpret_cast<float4*>(st + a_bytes + off) = lo;
     }
-    // B chunk: N rows (q) x 32 (pre-split on the host)
-    for (int idx = tid; idx < N * 8; idx += 128) {
+    // B chunk: N rows (q) x 16 (pre-split on the host)
+    for (int idx = tid; idx < N * 4; idx += 128) {
       const int w = idx >> 5, ln = idx & 31;         // same conflict-free mapping: 8 rows x 4 chunks per warp
-      const int q = ((w >> 1) * 8) + (ln & 7), c16 = (w & 1) * 4 + (ln >> 3);
+      const int q = w * 8 + (ln & 7), c16 = ln >> 3;
       const int j = j0 + 4 * c16;
       float4 h = make_float4(0.f, 0.f, 0.f, 0.f), lo = h;
       if (q < pk) {
@@ -201,7 +202,7 @@ radial_tc_kernel(const float* __restrict__ ghat, const float* __restrict__ t_hi,
         const uint32_t base = smem_u32(st);
         const uint32_t lbo_a = (TC_M / 8) * 128, lbo_b = uint32_t(N / 8) * 128;
 #pragma unroll
-        for (int s4 = 0; s4 < TC_KC / 8; ++s4) {
+        for (int s4 = 0; s4 < RK_KC / 8; ++s4) {
           const uint32_t ko_a = uint32_t(2 * s4) * lbo_a, ko_b = uint32_t(2 * s4) * lbo_b;
           const uint64_t ah = make_desc(base + ko_a, lbo_a, 128);
           const uint64_t al = make_desc(base + a_bytes + ko_a, lbo_a, 128);
@@ -216,7 +217,7 @@ radial_tc_kernel(const float* __restrict__ ghat, const float* __restrict__ t_hi,
       __syncwarp();
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) va[u] = vn[u];
+    for (int u = 0; u < 4; ++u) va[u] = vn[u];
   }
   // the last commit tracks every MMA issued before it
   mbar_wait(&bars[(nchunks - 1) & 1], ((nchunks - 1) >> 1) & 1);
@@ -241,7 +242,7 @@ radial_tc_kernel(const float* __restrict__ ghat, const float* __restrict__ t_hi,
 }
 
 int radial_tc_smem(int nmax) {
-  const int a_bytes = TC_M * TC_KC * 4, b_bytes = nmax * TC_KC * 4;
+  const int a_bytes = TC_M * RK_KC * 4, b_bytes = nmax * RK_KC * 4;
   return 2 * (2 * a_bytes + 2 * b_bytes) + 64;
 }
 
