@@ -159,6 +159,10 @@ fbspca_status upload_plan(Plan& P) {
   PolarParams& pp = P.pp;
   pp.xscratch_stride = (int64_t)P.L * pp.ncols_x;
   pp.pscratch_stride = (int64_t)P.n_xi * pp.half;
+  pp.ghat_kstride = 2 * P.max_batch * (int64_t)P.n_xi;
+  FB_CUDA(cudaStreamCreateWithFlags(&P.side, cudaStreamNonBlocking), "side stream");
+  FB_CUDA(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming), "fork event");
+  FB_CUDA(cudaEventCreateWithFlags(&P.ev_join, cudaEventDisableTiming), "join event");
   FB_CUDA(cudaMalloc(&P.d_xscratch, (size_t)P.polar_grid * pp.xscratch_stride * csz), "alloc xscratch");
   FB_CUDA(cudaMalloc(&P.d_pscratch, (size_t)P.polar_grid * pp.pscratch_stride * csz), "alloc pscratch");
   FB_CUDA(cudaMalloc(&P.d_ghat, (size_t)nk * P.max_batch * 2 * P.n_xi * rsz), "alloc ghat");
@@ -189,6 +193,9 @@ void free_plan(Plan& P) {
                   P.d_noderec};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& ev : P.tevents) { cudaEventDestroy(ev.second.first); cudaEventDestroy(ev.second.second); }
+  if (P.ev_fork) cudaEventDestroy(P.ev_fork);
+  if (P.ev_join) cudaEventDestroy(P.ev_join);
+  if (P.side) cudaStreamDestroy(P.side);
 }
 
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
@@ -273,7 +280,7 @@ fbspca_status fbspca_expand(fbspca_plan_t h, const void* d_images, int64_t n, vo
     }
     {
       TimedRegion t(P, T_RADIAL, s);
-      if (P.dt == FBSPCA_F32 && P.use_tc && P.n_xi % 4 == 0) FB_CUDA(launch_radial_tc(P, nb, b0, n, d_coeffs, s), "radial tc kernel");
+      if (P.dt == FBSPCA_F32 && P.use_tc && P.n_xi % 4 == 0) FB_CUDA(launch_radial_tma(P, nb, b0, n, d_coeffs, s), "radial tma kernel");
       else FB_CUDA(launch_radial(P, nb, b0, n, d_coeffs, s), "radial kernel");
     }
   }

@@ -13,8 +13,8 @@ namespace fbspca {
 
 constexpr int kMaxRadixStages = 16;
 constexpr int kMaxPhases = 64;
-constexpr int kCovChunk = 128;          // images per covariance split-K chunk (bounds fp32 accumulation length)
-constexpr int kCovBatch = 8192;         // images per covariance launch
+constexpr int kCovChunk = 1024;         // images per covariance split-K chunk (bounds fp32 accumulation length)
+constexpr int kCovBatch = 16384;        // images per covariance launch
 constexpr int kCovMaxChunks = kCovBatch / kCovChunk;
 
 // Stockham radix plan for a length-N FFT (N = prod radices; radices in {2,3,4,5,8}).
@@ -51,6 +51,7 @@ struct PolarParams {
   const int4* noderec;            // per entry {b1 | b2 << 16, t1, t2, (j << 16) | l} (fp32 path)
   void* xscratch;                 // per resident CTA: L x ncols_x complex
   void* pscratch;                 // per resident CTA: n_xi x half complex
+  int64_t ghat_kstride;           // ghat elements (T) per k: 2 max_batch n_xi (fixed, so one TMA map serves all batches)
   int64_t xscratch_stride, pscratch_stride;   // complex elements per CTA
 };
 
@@ -98,7 +99,7 @@ struct Plan {
   PolarParams* d_pp = nullptr;           // device copy of pp
   void* d_xscratch = nullptr;
   void* d_pscratch = nullptr;
-  void* d_ghat = nullptr;                // (k_max+1) x max_batch x 2 x n_xi  (T)
+  void* d_ghat = nullptr;                // (k_max+1) x max_batch x 2 x n_xi  (T), k stride 2 max_batch n_xi
   double* d_partial = nullptr;           // blk_off[k_max+1] + p_0 + 1
   double* d_cov_scratch = nullptr;       // kCovMaxChunks x (blk_off[k_max+1] + p_0 + 1)
   int* d_coef_k = nullptr;               // row -> k lookup (coef rows)
@@ -115,6 +116,8 @@ struct Plan {
   std::vector<float> tms;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> tevents;
   int num_sms = 0;
+  cudaStream_t side = nullptr;           // K5: the k = 0 fp64 CTAs run here, forked from / joined to the caller's stream
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 // ---- host plan construction (plan.cpp) ----
@@ -136,9 +139,9 @@ cudaError_t launch_project(const Plan& P, const void* d_coeffs, int64_t n, const
                            const double* d_evals, const double* d_evecs, double sigma2, int mode,
                            int64_t n_total, void* d_out, cudaStream_t s);
 int polar_max_smem();
-cudaError_t launch_radial_tc(const Plan& P, int64_t nb, int64_t i0, int64_t ld, void* d_coeffs, cudaStream_t s);
-cudaError_t launch_cov_tc(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb, cudaStream_t s);
-int radial_tc_cols(int pmax);
+cudaError_t launch_radial_tma(const Plan& P, int64_t nb, int64_t i0, int64_t ld, void* d_coeffs, cudaStream_t s);
+cudaError_t launch_cov_tma(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb, cudaStream_t s);
+cudaError_t launch_cov_k0(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb, cudaStream_t s);
 int fft_values_per_lane(const FftPlan& f);
 int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps);
 

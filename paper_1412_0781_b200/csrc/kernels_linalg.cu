@@ -14,7 +14,7 @@ namespace fbspca {
 template <typename T>
 __global__ void __launch_bounds__(256)
 radial_kernel(const T* __restrict__ ghat, const T* __restrict__ table, const int* __restrict__ p,
-              const int64_t* __restrict__ coef_off, int nb, int n_xi, int64_t i0, int64_t ld,
+              const int64_t* __restrict__ coef_off, int nb, int n_xi, int64_t kstride, int64_t i0, int64_t ld,
               T* __restrict__ out) {
   constexpr int BM = 64, BN = 64, BK = 32;
   __shared__ T As[BK][BM + 1];
@@ -26,7 +26,7 @@ radial_kernel(const T* __restrict__ ghat, const T* __restrict__ table, const int
   const int rows = 2 * nb;
   const int r0 = blockIdx.x * BM;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const T* A = ghat + (int64_t)k * rows * n_xi;
+  const T* A = ghat + (int64_t)k * kstride;
   const T* B = table + coef_off[k] * n_xi;
   T acc[4][4];
 #pragma unroll
@@ -73,10 +73,11 @@ cudaError_t launch_radial(const Plan& P, int64_t nb, int64_t i0, int64_t ld, voi
   dim3 grid((unsigned)((2 * nb + 63) / 64), (unsigned)(P.k_max + 1), (unsigned)((pmax + 63) / 64));
   if (P.dt == FBSPCA_F32)
     radial_kernel<float><<<grid, 256, 0, s>>>((const float*)P.d_ghat, (const float*)P.d_table, P.d_p, P.d_coef_off,
-                                              (int)nb, P.n_xi, i0, ld, (float*)d_coeffs);
+                                              (int)nb, P.n_xi, P.pp.ghat_kstride, i0, ld, (float*)d_coeffs);
   else
     radial_kernel<double><<<grid, 256, 0, s>>>((const double*)P.d_ghat, (const double*)P.d_table, P.d_p,
-                                               P.d_coef_off, (int)nb, P.n_xi, i0, ld, (double*)d_coeffs);
+                                               P.d_coef_off, (int)nb, P.n_xi, P.pp.ghat_kstride, i0, ld,
+                                               (double*)d_coeffs);
   return cudaGetLastError();
 }
 
@@ -181,12 +182,15 @@ cudaError_t launch_cov_accum(const Plan& P, const void* d_coeffs, int64_t ld, in
   if (nchunk > kCovMaxChunks) return cudaErrorInvalidValue;
   const int64_t total = P.blk_off[P.k_max + 1] + P.p[0] + 1;
   dim3 grid((unsigned)(P.k_max + 1), (unsigned)(nt * (nt + 1) / 2), (unsigned)nchunk);
-  if (P.dt == FBSPCA_F32 && P.use_tc && P.p[0] <= 256 && (ld % 2) == 0) {   // float4 rows need even ld
-    // k >= 1 on the tensor cores; k = 0 (uncentred, mean^2/var ~ 10: F9) accumulates in fp64 on CUDA cores
-    dim3 g0(1u, (unsigned)(nt * (nt + 1) / 2), (unsigned)nchunk);
-    cov_accum_kernel<float><<<g0, 256, 0, s>>>((const float*)d_coeffs, P.d_p, P.d_coef_off, P.d_blk_off, ld, i0, nb,
-                                               P.k_max, P.d_cov_scratch, total);
-    cudaError_t e = launch_cov_tc(P, d_coeffs, ld, i0, nb, s);
+  if (P.dt == FBSPCA_F32 && P.use_tc && P.k_max >= 1 && ((P.p[1] + 15) & ~15) <= 128 && (ld % 2) == 0) {
+    // k >= 1 on the tensor cores (TMA-fed, persistent); k = 0 (uncentred, mean^2/var ~ 10: F9) in fp64 on the
+    // CUDA cores, forked onto the plan's side stream so the two overlap
+    cudaError_t e = cudaEventRecord(P.ev_fork, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(P.side, P.ev_fork, 0);
+    if (e == cudaSuccess) e = launch_cov_k0(P, d_coeffs, ld, i0, nb, P.side);
+    if (e == cudaSuccess) e = cudaEventRecord(P.ev_join, P.side);
+    if (e == cudaSuccess) e = launch_cov_tma(P, d_coeffs, ld, i0, nb, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, P.ev_join, 0);
     if (e != cudaSuccess) return e;
   } else if (P.dt == FBSPCA_F32)
     cov_accum_kernel<float><<<grid, 256, 0, s>>>((const float*)d_coeffs, P.d_p, P.d_coef_off, P.d_blk_off, ld, i0, nb,

@@ -497,7 +497,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       PROF_MARK(4);
       {
         // warp per k: lanes write rings j0 + lane (re row then im row), 128-B coalesced stores
-        const int64_t kstride = n_img * 2 * (int64_t)n_xi;
+        const int64_t kstride = pp.ghat_kstride;
         // g <= 16: each half-warp writes one k (two k per warp instruction); else a warp per k
         const int per = g <= 16 ? 2 : 1;
         const int sub = per == 2 ? (lane >> 4) : 0, ln = per == 2 ? (lane & 15) : lane, lstep = per == 2 ? 16 : 32;
