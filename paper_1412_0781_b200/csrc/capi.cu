@@ -169,6 +169,8 @@ fbspca_status upload_plan(Plan& P) {
   const int64_t npart = P.blk_off[nk] + P.p[0] + 1;
   FB_CUDA(cudaMalloc((void**)&P.d_partial, npart * sizeof(double)), "alloc partial");
   FB_CUDA(cudaMalloc((void**)&P.d_cov_scratch, (size_t)kCovMaxChunks * npart * sizeof(double)), "alloc cov scratch");
+  FB_CUDA(cudaMalloc((void**)&P.d_cov_scratch0, (size_t)kCovMaxSub0 * (P.blk_off[1] + P.p[0] + 1) * sizeof(double)),
+          "alloc cov scratch0");
   FB_CUDA(upload((void**)&P.d_p, P.p.data(), P.p.size()), "upload p");
   FB_CUDA(upload((void**)&P.d_coef_off, P.coef_off.data(), P.coef_off.size()), "upload coef_off");
   FB_CUDA(upload((void**)&P.d_blk_off, P.blk_off.data(), P.blk_off.size()), "upload blk_off");
@@ -189,7 +191,7 @@ void free_plan(Plan& P) {
   DeviceGuard g(P.device);
   void* ptrs[] = {P.d_table, P.d_deapod, P.d_tw_M, P.d_tw_theta, P.d_rho, P.d_cs, P.d_nodes, P.d_xscratch,
                   P.d_pscratch, P.d_ghat, P.d_partial, P.d_p, P.d_coef_off, P.d_blk_off, P.d_evec_off,
-                  P.d_eig_work, P.d_eig_sweeps, P.d_coef_k, P.d_pp, P.d_cov_scratch, P.d_table_hi, P.d_table_lo,
+                  P.d_eig_work, P.d_eig_sweeps, P.d_coef_k, P.d_pp, P.d_cov_scratch, P.d_cov_scratch0, P.d_table_hi, P.d_table_lo,
                   P.d_noderec};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& ev : P.tevents) { cudaEventDestroy(ev.second.first); cudaEventDestroy(ev.second.second); }

@@ -16,6 +16,8 @@ constexpr int kMaxPhases = 64;
 constexpr int kCovChunk = 1024;         // images per covariance split-K chunk (bounds fp32 accumulation length)
 constexpr int kCovBatch = 16384;        // images per covariance launch
 constexpr int kCovMaxChunks = kCovBatch / kCovChunk;
+constexpr int kCovChunk0 = 128;         // images per k = 0 fp64 CTA (tensor-core path: its own scratch, more CTAs)
+constexpr int kCovMaxSub0 = kCovBatch / kCovChunk0;
 
 // Stockham radix plan for a length-N FFT (N = prod radices; radices in {2,3,4,5,8}).
 struct FftPlan {
@@ -102,6 +104,7 @@ struct Plan {
   void* d_ghat = nullptr;                // (k_max+1) x max_batch x 2 x n_xi  (T), k stride 2 max_batch n_xi
   double* d_partial = nullptr;           // blk_off[k_max+1] + p_0 + 1
   double* d_cov_scratch = nullptr;       // kCovMaxChunks x (blk_off[k_max+1] + p_0 + 1)
+  double* d_cov_scratch0 = nullptr;      // kCovMaxSub0 x (blk_off[1] + p_0 + 1): k = 0 block, s_0, count
   int* d_coef_k = nullptr;               // row -> k lookup (coef rows)
   int* d_p = nullptr;
   int64_t* d_coef_off = nullptr;

@@ -166,11 +166,20 @@ cov_accum_kernel(const T* __restrict__ coeffs, const int* __restrict__ p, const 
   }
 }
 
+// partial[i] += sum over chunks (fixed order).  nsub0 > 0: the k = 0 block [0, blk1) and s_0/count [s0_at, total)
+// come from scratch0 (nsub0 sub-chunks of stride0 = blk1 + p_0 + 1, s_0 at blk1) instead of scratch.
 __global__ void cov_reduce_kernel(const double* __restrict__ scratch, int64_t stride, int nchunk, int64_t total,
+                                  const double* __restrict__ scratch0, int nsub0, int64_t blk1, int64_t s0_at,
                                   double* __restrict__ partial) {
+  const int64_t stride0 = blk1 + (total - s0_at);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     double s = partial[i];
-    for (int c = 0; c < nchunk; ++c) s += scratch[(int64_t)c * stride + i];
+    if (nsub0 > 0 && (i < blk1 || i >= s0_at)) {
+      const int64_t j = i < blk1 ? i : blk1 + (i - s0_at);
+      for (int c = 0; c < nsub0; ++c) s += scratch0[(int64_t)c * stride0 + j];
+    } else {
+      for (int c = 0; c < nchunk; ++c) s += scratch[(int64_t)c * stride + i];
+    }
     partial[i] = s;
   }
 }
@@ -182,7 +191,8 @@ cudaError_t launch_cov_accum(const Plan& P, const void* d_coeffs, int64_t ld, in
   if (nchunk > kCovMaxChunks) return cudaErrorInvalidValue;
   const int64_t total = P.blk_off[P.k_max + 1] + P.p[0] + 1;
   dim3 grid((unsigned)(P.k_max + 1), (unsigned)(nt * (nt + 1) / 2), (unsigned)nchunk);
-  if (P.dt == FBSPCA_F32 && P.use_tc && P.k_max >= 1 && ((P.p[1] + 15) & ~15) <= 128 && (ld % 2) == 0) {
+  const bool tc = P.dt == FBSPCA_F32 && P.use_tc && P.k_max >= 1 && ((P.p[1] + 15) & ~15) <= 128 && (ld % 2) == 0;
+  if (tc) {
     // k >= 1 on the tensor cores (TMA-fed, persistent); k = 0 (uncentred, mean^2/var ~ 10: F9) in fp64 on the
     // CUDA cores, forked onto the plan's side stream so the two overlap
     cudaError_t e = cudaEventRecord(P.ev_fork, s);
@@ -201,7 +211,9 @@ cudaError_t launch_cov_accum(const Plan& P, const void* d_coeffs, int64_t ld, in
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4 * 148);
-  cov_reduce_kernel<<<blocks, 256, 0, s>>>(P.d_cov_scratch, total, nchunk, total, d_partial);
+  cov_reduce_kernel<<<blocks, 256, 0, s>>>(P.d_cov_scratch, total, nchunk, total, P.d_cov_scratch0,
+                                           tc ? (int)((nb + kCovChunk0 - 1) / kCovChunk0) : 0, P.blk_off[1],
+                                           P.blk_off[P.k_max + 1], d_partial);
   return cudaGetLastError();
 }
 

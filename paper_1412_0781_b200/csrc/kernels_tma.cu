@@ -126,9 +126,10 @@ __device__ __forceinline__ int pow2_cols(int c) { int t = 32; while (t < c) t <<
 
 // ---------------------------------------------------------------- K4
 // Work item = (k, row tile of 128 rows of the batch); items are dealt round-robin to the persistent CTAs.
-// Stage = A chunk (128 rows x 32 j, 16 KB, TMA) + its lo part (16 KB) + B = [T_hi (b rows) ; T_lo (b rows)],
-// b = the smallest TMA box >= roundup16(p_k).  b <= 128: 2 MMAs of N = 2b per K step, D[q] + D[b + q];
-// b = 256 (p_k > 128): 3 MMAs of N = b (x_raw T_hi, x_raw T_lo, x_lo T_hi).
+// Stage = A chunk (128 rows x 32 j, 16 KB, TMA) + B = [T_hi (b rows) ; T_lo (b rows)], b = the smallest TMA box
+// >= roundup16(p_k); the lo part of A goes to a separate 2-deep ring (so more A is in flight per SM).
+// b <= 128: 2 MMAs of N = 2b per K step, D[q] + D[b + q]; b = 256 (p_k > 128): 3 MMAs of N = b
+// (x_raw T_hi, x_raw T_lo, x_lo T_hi).  Warps: 0-3 lo parts, 4 TMA, 5 MMA, 6-9 epilogue (TMEM lane quarter w % 4).
 struct K4Args {
   int k_max, n_xi, nrt, rows, nkc, stages, bmax;   // bmax = largest box b of the plan
   int64_t ghat_krows;                               // ghat rows per k (2 max_batch)
@@ -138,18 +139,20 @@ struct K4Args {
   float* out;
 };
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
 radial_tma_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ MapSet tm_bh,
                   const __grid_constant__ MapSet tm_bl, const K4Args args) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
   const int NS = args.stages;
   const uint32_t a_bytes = 128 * ROWB, b_bytes = uint32_t(args.bmax) * ROWB;
-  const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;           // A, lo(A), T_hi, T_lo
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + NS * stage_bytes);
-  uint64_t* loready = full + NS;
-  uint64_t* empty = loready + NS;
-  uint64_t* accfull = empty + NS;                                   // 2
+  const uint32_t stage_bytes = a_bytes + 2 * b_bytes;               // A, T_hi, T_lo
+  unsigned char* lo_ring = sm + NS * stage_bytes;                   // 2 x a_bytes
+  uint64_t* full = reinterpret_cast<uint64_t*>(lo_ring + 2 * a_bytes);
+  uint64_t* empty = full + NS;
+  uint64_t* loready = empty + NS;                                   // 2
+  uint64_t* lofree = loready + 2;                                   // 2
+  uint64_t* accfull = lofree + 2;                                   // 2
   uint64_t* accempty = accfull + 2;                                 // 2
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -158,8 +161,10 @@ radial_tma_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constan
 
   if (warp == 0) tmem_alloc(tmem_slot, tcols);
   if (tid == 0) {
-    for (int s = 0; s < NS; ++s) { bar_init(&full[s], 1); bar_init(&loready[s], 128); bar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { bar_init(&accfull[a], 1); bar_init(&accempty[a], 128); }
+    for (int s = 0; s < NS; ++s) { bar_init(&full[s], 1); bar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) {
+      bar_init(&loready[a], 128); bar_init(&lofree[a], 1); bar_init(&accfull[a], 1); bar_init(&accempty[a], 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -183,8 +188,8 @@ radial_tma_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constan
           unsigned char* st = sm + s * stage_bytes;
           bar_expect_tx(&full[s], a_bytes + 2u * uint32_t(b) * ROWB);
           tma_2d(st, &tm_a, kc * KC, arow, &full[s]);
-          tma_2d(st + 2 * a_bytes, &tm_bh.m[bi], kc * KC, brow, &full[s]);
-          tma_2d(st + 2 * a_bytes + b * ROWB, &tm_bl.m[bi], kc * KC, brow, &full[s]);
+          tma_2d(st + a_bytes, &tm_bh.m[bi], kc * KC, brow, &full[s]);
+          tma_2d(st + a_bytes + b * ROWB, &tm_bl.m[bi], kc * KC, brow, &full[s]);
         }
       }
     }
@@ -203,10 +208,12 @@ radial_tma_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constan
         bar_wait(&accempty[a], ((t >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         for (int kc = 0; kc < args.nkc; ++kc, ++it) {
-          const int s = it % NS;
-          bar_wait(&loready[s], (it / NS) & 1);
+          const int s = it % NS, l = it & 1;
+          bar_wait(&full[s], (it / NS) & 1);
+          bar_wait(&loready[l], (it >> 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t xa = su32(sm + s * stage_bytes), xl = xa + a_bytes, bh = xa + 2 * a_bytes, bl = bh + b * ROWB;
+          const uint32_t xa = su32(sm + s * stage_bytes), bh = xa + a_bytes, bl = bh + b * ROWB;
+          const uint32_t xl = su32(lo_ring + l * a_bytes);
 #pragma unroll
           for (int s4 = 0; s4 < KC / 8; ++s4) {
             const uint32_t ko = uint32_t(s4) * 32u;                 // 8 tf32 = 32 B along the swizzled row
@@ -221,60 +228,62 @@ radial_tma_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constan
             }
           }
           mma_commit(&empty[s]);
+          mma_commit(&lofree[l]);
         }
         mma_commit(&accfull[a]);
       }
     }
     return;
   }
-  // ---- warps 0-3: lo parts of every chunk; the epilogue of item t runs after the lo parts of item t+1
-  auto epilogue = [&](int t, int item) {
-    const int k = item / args.nrt, rt = item - k * args.nrt;
-    const int pk = args.p[k];
-    const int b = 16 << box_idx((pk + 15) & ~15);
-    const bool cat = b <= 128;
-    const int a = t & 1;
-    bar_wait(&accfull[a], (t >> 1) & 1);
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    const int row = rt * 128 + 32 * warp + lane;
-    const int64_t base = args.coef_off[k];
-    float* o = args.out + 2 * args.i0 + row;
-    const uint32_t tbase = tmem + (uint32_t(32 * warp) << 16) + uint32_t(a * acc_cols);
-    for (int q0 = 0; q0 < pk; q0 += 16) {
-      float v[16];
-      tmem_ld16(tbase + uint32_t(q0), v);
-      if (cat) {
-        float w[16];
-        tmem_ld16(tbase + uint32_t(b + q0), w);
+  if (warp >= 6) {                                                  // ---- epilogue: TMEM lanes 32 (w % 4) ..
+    const int wq = warp & 3;
+    int t = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
+      const int k = item / args.nrt, rt = item - k * args.nrt;
+      const int pk = args.p[k];
+      const int b = 16 << box_idx((pk + 15) & ~15);
+      const bool cat = b <= 128;
+      const int a = t & 1;
+      bar_wait(&accfull[a], (t >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int row = rt * 128 + 32 * wq + lane;
+      const int64_t base = args.coef_off[k];
+      float* o = args.out + 2 * args.i0 + row + base * 2 * args.ld;
+      const uint32_t tbase = tmem + (uint32_t(32 * wq) << 16) + uint32_t(a * acc_cols);
+      const bool zero = (k == 0 && (row & 1));
+      for (int q0 = 0; q0 < pk; q0 += 16) {
+        float v[16];
+        tmem_ld16(tbase + uint32_t(q0), v);
+        if (cat) {
+          float w[16];
+          tmem_ld16(tbase + uint32_t(b + q0), w);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] += w[i];
-      }
-      if (row < args.rows) {
+          for (int i = 0; i < 16; ++i) v[i] += w[i];
+        }
+        if (row < args.rows) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int q = q0 + i;
-          if (q < pk) o[(base + q) * 2 * args.ld] = (k == 0 && (row & 1)) ? 0.f : v[i];
+          for (int i = 0; i < 16; ++i)
+            if (q0 + i < pk) __stcs(o + (int64_t)(q0 + i) * 2 * args.ld, zero ? 0.f : v[i]);
         }
       }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      bar_arrive(&accempty[a]);
     }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    bar_arrive(&accempty[a]);
-  };
-  int it = 0, t = 0, prev_item = -1;
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
-    for (int kc = 0; kc < args.nkc; ++kc, ++it) {
-      const int s = it % NS;
-      unsigned char* st = sm + s * stage_bytes;
-      bar_wait(&full[s], (it / NS) & 1);
-      make_lo(st, st + a_bytes, a_bytes, tid);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      bar_arrive(&loready[s]);
-    }
-    if (prev_item >= 0) epilogue(t - 1, prev_item);
-    prev_item = item;
+    named_sync(2, 256);                                             // TMEM reads done before the dealloc
+    return;
   }
-  if (prev_item >= 0) epilogue(t - 1, prev_item);
-  named_sync(1, 128);
+  // ---- warps 0-3: lo parts of every chunk into the 2-deep lo ring
+  int it = 0;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x)
+    for (int kc = 0; kc < args.nkc; ++kc, ++it) {
+      const int s = it % NS, l = it & 1;
+      bar_wait(&full[s], (it / NS) & 1);
+      bar_wait(&lofree[l], ((it >> 1) & 1) ^ 1);
+      make_lo(sm + s * stage_bytes, lo_ring + l * a_bytes, a_bytes, tid);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bar_arrive(&loready[l]);
+    }
+  named_sync(2, 256);
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
 }
 
@@ -505,9 +514,9 @@ cudaError_t launch_radial_tma(const Plan& P, int64_t nb, int64_t i0, int64_t ld,
   a.p = P.d_p; a.coef_off = P.d_coef_off; a.out = reinterpret_cast<float*>(d_coeffs);
   const int bbox = bmax <= 16 ? 16 : bmax <= 32 ? 32 : bmax <= 64 ? 64 : bmax <= 128 ? 128 : 256;
   a.bmax = bbox;                                           // B tiles sized for the largest box
-  const int stage = 2 * 128 * ROWB + 2 * bbox * ROWB;
-  const int fixed = 1024 + 256;
-  a.stages = std::max(2, std::min(6, (227 * 1024 - fixed) / stage));
+  const int stage = 128 * ROWB + 2 * bbox * ROWB;
+  const int fixed = 2 * 128 * ROWB + 1024 + 256;
+  a.stages = std::max(2, std::min(8, (227 * 1024 - fixed) / stage));
   const int smem = a.stages * stage + fixed;
   static int configured = 0;
   if (configured < smem) {
@@ -517,7 +526,7 @@ cudaError_t launch_radial_tma(const Plan& P, int64_t nb, int64_t i0, int64_t ld,
   }
   const int items = nk * a.nrt;
   const int grid = std::min(items, P.num_sms);
-  radial_tma_kernel<<<grid, 192, smem, s>>>(ta, tbh, tbl, a);
+  radial_tma_kernel<<<grid, 320, smem, s>>>(ta, tbh, tbl, a);
   return cudaGetLastError();
 }
 
@@ -625,12 +634,13 @@ cov_k0_kernel(const float* __restrict__ A0, int pk, int64_t ld, int64_t i0, int6
   }
 }
 
+// scratch0[sub] = [packed k = 0 block | s_0 | count] per kCovChunk0 images
 cudaError_t launch_cov_k0(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb, cudaStream_t s) {
   const int nt = (P.p[0] + 63) / 64;
-  dim3 grid((unsigned)(nt * (nt + 1) / 2), (unsigned)((nb + kCovChunk - 1) / kCovChunk));
-  const int64_t stride = P.blk_off[P.k_max + 1] + P.p[0] + 1;
+  dim3 grid((unsigned)(nt * (nt + 1) / 2), (unsigned)((nb + kCovChunk0 - 1) / kCovChunk0));
+  const int64_t stride = P.blk_off[1] + P.p[0] + 1;
   cov_k0_kernel<<<grid, 128, 0, s>>>(reinterpret_cast<const float*>(d_coeffs) + P.coef_off[0] * 2 * ld, P.p[0], ld, i0,
-                                     nb, kCovChunk, P.blk_off[0], P.blk_off[P.k_max + 1], P.d_cov_scratch, stride);
+                                     nb, kCovChunk0, 0, P.blk_off[1], P.d_cov_scratch0, stride);
   return cudaGetLastError();
 }
 
