@@ -5,6 +5,8 @@
 // are product-only (the oracle uses a direct Fourier sum).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -104,6 +106,88 @@ FftPlan make_fft(int n) {
 }
 
 int ceil_guard(double x) { return int(std::ceil(x - 1e-9)); }   // reading Q4
+
+// Warp packing of the gather's node pairs (shared-memory bank model of K2's 6 x 6 tap loads).
+// Lane i of a warp reads grid words (b1_i + q + row0) S + b2_i + c (node A) and (row0 - b1_i - q) S + b2_i + c
+// (mirrored node B) for every tap (q, c): 64-bit words, 16 word-wide bank pairs, served per half-warp.  The tap
+// offset is common to all lanes, so a half-warp's load costs max over bank pairs of the number of DISTINCT
+// anchors in that pair, for classes cA = (b1 S + b2) mod 16 and cB = (b2 - b1 S) mod 16 -- 1 wavefront when the
+// 16 lanes' distinct anchors fall in distinct pairs (equal anchors broadcast).  This model reproduces ncu's
+// count for the plain (b1, b2) order at C3 (106.7k vs 102k wavefronts/image measured).  Greedy: walk anchors in
+// (b1, b2) order, put an anchor into the open half-warp if neither class is at the cap (equal anchors are
+// free), skip it otherwise; the cap doubles only when nothing left in the window fits.  Groups are emitted
+// full (16) except the phase's last.
+
+// Model cost (wavefronts per tap, summed over warps) of a node order under the bank model above.
+long gather_bank_cost(const std::vector<uint32_t>& ord, const std::vector<double>& rho, const std::vector<double>& cs,
+                      double hw, int S, int half, int group = 32) {
+  long tot = 0;
+  for (size_t w0 = 0; w0 < ord.size(); w0 += group) {
+    std::vector<std::pair<int, int>> a, b;
+    for (size_t i = w0; i < std::min(ord.size(), w0 + group); ++i) {
+      const int j = int(ord[i] >> 16), l = int(ord[i] & 0xffffu);
+      const int b1 = int(std::ceil(rho[j] * cs[2 * l] - hw)), b2 = int(std::ceil(rho[j] * cs[2 * l + 1] - hw));
+      a.push_back({b1, b2});
+      if (l != 0 && 2 * l != half) b.push_back({b1, b2});
+    }
+    for (int sg = 1; sg >= -1; sg -= 2) {
+      auto& v = sg == 1 ? a : b;
+      std::sort(v.begin(), v.end());
+      v.erase(std::unique(v.begin(), v.end()), v.end());
+      int cnt[16] = {0}, m = 0;
+      for (auto& e : v) m = std::max(m, ++cnt[(((sg * e.first * S + e.second) % 16) + 16) % 16]);
+      tot += m;
+    }
+  }
+  return tot;
+}
+
+std::vector<uint32_t> pack_gather_warps(const std::vector<uint32_t>& nodes, const std::vector<double>& rho,
+                                        const std::vector<double>& cs, double hw, int S) {
+  struct Anc { int b1, b2; std::vector<uint32_t> ids; };
+  std::vector<Anc> anc;
+  {
+    std::vector<std::pair<std::pair<int, int>, uint32_t>> keyed;
+    keyed.reserve(nodes.size());
+    for (uint32_t nd : nodes) {
+      const int j = int(nd >> 16), l = int(nd & 0xffffu);
+      const double k1 = rho[j] * cs[2 * l], k2 = rho[j] * cs[2 * l + 1];
+      keyed.push_back({{int(std::ceil(k1 - hw)), int(std::ceil(k2 - hw))}, nd});
+    }
+    std::sort(keyed.begin(), keyed.end());
+    for (auto& e : keyed) {
+      if (anc.empty() || anc.back().b1 != e.first.first || anc.back().b2 != e.first.second)
+        anc.push_back({e.first.first, e.first.second, {}});
+      anc.back().ids.push_back(e.second);
+    }
+  }
+  auto cls = [&](int b1, int b2, int sgn) { return (((sgn * b1 * S + b2) % 16) + 16) % 16; };
+  std::vector<uint32_t> out;
+  out.reserve(nodes.size());
+  std::vector<char> used(anc.size(), 0);
+  std::vector<size_t> done_ids(anc.size(), 0);
+  size_t next = 0, left = anc.size();
+  while (left > 0) {
+    int cntA[16] = {0}, cntB[16] = {0}, slots = 16;
+    for (int cap = 1; slots > 0 && left > 0 && cap <= 16; cap *= 2) {
+      size_t scanned = 0;
+      for (size_t a = next; a < anc.size() && slots > 0 && scanned < 4096; ++a) {
+        if (used[a]) continue;
+        ++scanned;
+        const int ca = cls(anc[a].b1, anc[a].b2, 1), cb = cls(anc[a].b1, anc[a].b2, -1);
+        if (cntA[ca] >= cap || cntB[cb] >= cap) continue;
+        ++cntA[ca]; ++cntB[cb];
+        const size_t take = std::min<size_t>(anc[a].ids.size() - done_ids[a], size_t(slots));
+        for (size_t t = 0; t < take; ++t) out.push_back(anc[a].ids[done_ids[a] + t]);
+        done_ids[a] += take;
+        slots -= int(take);
+        if (done_ids[a] == anc[a].ids.size()) { used[a] = 1; --left; }
+      }
+      while (next < anc.size() && used[next]) ++next;
+    }
+  }
+  return out;
+}
 
 }  // namespace
 
@@ -261,20 +345,21 @@ fbspca_status build_host_plan(Plan& P) {
       // pair leaders only: node (j, half - l) = (-k1, k2) is gathered with (j, l) (same columns)
       if (2 * l <= half) ph.push_back((uint32_t(j) << 16) | uint32_t(l));
     }
-    // Order for the gather's shared-memory accesses: by row anchor b1, then column anchor b2, so a warp's
-    // lanes read the same grid rows at neighbouring columns (ring-major order: ~2x ideal wavefronts;
-    // (b1, b2) order: ~1.5x).
-    auto key = [&](uint32_t nd) {
-      const int j = int(nd >> 16), l = int(nd & 0xffffu);
-      const double k1 = rho[j] * cs[2 * l], k2 = rho[j] * cs[2 * l + 1];
-      return std::make_pair(int(std::ceil(k1 - hw)), int(std::ceil(k2 - hw)));
-    };
-    std::sort(ph.begin(), ph.end(), [&](uint32_t x, uint32_t y) {
-      auto kx = key(x), ky = key(y);
-      return kx != ky ? kx < ky : x < y;
-    });
-    // (Measured: dealing a row's entries round-robin over b2 mod 16 removes slot collisions but is slower
-    // on B200 -- 145k vs 122k cycles/image for the C3 gather -- so the plain (b1, b2) order is kept.)
+    {
+      std::vector<uint32_t> packed = pack_gather_warps(ph, rho, cs, hw, S);
+      if (getenv("FBSPCA_DEBUG_PLAN")) {
+        std::vector<uint32_t> srt = ph;
+        auto key = [&](uint32_t nd) {
+          const int j = int(nd >> 16), l = int(nd & 0xffffu);
+          return std::make_pair(int(std::ceil(rho[j] * cs[2 * l] - hw)), int(std::ceil(rho[j] * cs[2 * l + 1] - hw)));
+        };
+        std::stable_sort(srt.begin(), srt.end(), [&](uint32_t x, uint32_t y) { return key(x) < key(y); });
+        fprintf(stderr, "phase %d: %zu pairs, half-warp bank model wavefronts/tap: (b1,b2)-sorted %ld, packed %ld, "
+                "floor %zu\n", np, ph.size(), gather_bank_cost(srt, rho, cs, hw, S, half, 16),
+                gather_bank_cost(packed, rho, cs, hw, S, half, 16), 2 * ((ph.size() + 15) / 16));
+      }
+      ph.swap(packed);
+    }
     P.nodes.insert(P.nodes.end(), ph.begin(), ph.end());
     ++np;
     lo = lo + S - w + 1;
