@@ -310,7 +310,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
     const T* gd = reinterpret_cast<const T*>(pp.deapod);
     if constexpr (MC > 0) {
       build_stage_tw<T2, MC>(twM, gtM, tid, nthr);             // per-stage tables (<= M entries)
-      build_stage_tw<T2, NC>(twT, gtT, tid, nthr);
+      for (int i = tid; i < NC / 2; i += nthr) twT[i] = gtT[i];   // ring pairs: e^{-2 pi i t / n_theta}, t < n/2
     } else {
       for (int i = tid; i < M; i += nthr) twM[i] = gtM[i];
       for (int i = tid; i < nt; i += nthr) twT[i] = gtT[i];
@@ -475,12 +475,55 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       PROF_MARK(3);
     }
 
-    // ---------------- K3: ring FFTs (full ring rebuilt from the half ring), staged [k][jj], written k-major
-    T2* stg = region + (size_t)pp.ang_warps * 2 * NTP;
+    // ---------------- K3: ring FFTs, staged [k][jj], written k-major.
+    // pow2 plans: ring pairs (j, j+1) per warp as two half-length (N = n_theta/2) FFTs.  With f the half ring and
+    // w = e^{-2 pi i / n_theta}, ghat(k) = sum_{l<N} [f_l + (-1)^k conj f_l] w^{kl}, so
+    //   even k = 2m: U = DFT_N(Re f_j + i Re f_j'),          ghat_j = U(m) + conj U(-m),   ghat_j' = -i (U(m) - conj U(-m))
+    //   odd k = 2m+1: V = DFT_N((Im f_j + i Im f_j') w^l),   ghat_j = i (V(m) + conj V(N-1-m)), ghat_j' = V(m) - conj V(N-1-m)
+    // (the real-input pair trick on each parity; w^l shifts the odd frequencies onto the N-point grid).
+    // Runtime sizes: one full n_theta-point FFT per ring rebuilt from the half ring.
+    T2* stg = (MC > 0) ? region : region + (size_t)pp.ang_warps * 2 * NTP;
     const int GS = G | 1;                            // odd staging stride (bank spread)
     for (int j0 = 0; j0 < n_xi; j0 += G) {
       const int g = min(G, n_xi - j0);
-      if (warp < pp.ang_warps) {
+      if constexpr (MC > 0) {
+        const int kmx = pp.k_max;
+        T2* res = fft_result_in_A<MC>() ? myA : myB;
+        auto stR = [res](int i, T2 v) { res[padi(i)] = v; };
+        for (int pr = warp; warp < pp.fft_warps && 2 * pr < g; pr += pp.fft_warps) {
+          const int jj = 2 * pr;
+          const bool two = jj + 1 < g;
+          const T2* fa = Pol + (int64_t)(j0 + jj) * half;
+          const T2* fb = two ? fa + half : fa;
+          auto ldu = [&](int t) -> T2 { const T2 a = fa[t], b = fb[t]; return T2{a.x, two ? b.x : T(0)}; };
+          fft_pow2<T2, MC>(ldu, stR, myA, myB, twM, lane);
+          __syncwarp();
+          for (int m = lane; 2 * m <= kmx; m += 32) {
+            const T2 u = res[padi(m)];
+            T2 uc = res[padi((MC - m) & (MC - 1))];
+            uc.y = -uc.y;
+            const T2 sp = cadd(u, uc), dm = csub(u, uc);
+            stg[(size_t)(2 * m) * GS + jj] = sp;
+            if (two) stg[(size_t)(2 * m) * GS + jj + 1] = T2{dm.y, -dm.x};
+          }
+          __syncwarp();
+          auto ldv = [&](int t) -> T2 {
+            const T2 a = fa[t], b = fb[t];
+            return cmul(T2{a.y, two ? b.y : T(0)}, twT[t]);
+          };
+          fft_pow2<T2, MC>(ldv, stR, myA, myB, twM, lane);
+          __syncwarp();
+          for (int m = lane; 2 * m + 1 <= kmx; m += 32) {
+            const T2 v = res[padi(m)];
+            T2 vc = res[padi(MC - 1 - m)];
+            vc.y = -vc.y;
+            const T2 sp = cadd(v, vc), dm = csub(v, vc);
+            stg[(size_t)(2 * m + 1) * GS + jj] = T2{-sp.y, sp.x};
+            if (two) stg[(size_t)(2 * m + 1) * GS + jj + 1] = dm;
+          }
+          __syncwarp();
+        }
+      } else if (warp < pp.ang_warps) {
         for (int jj = warp; jj < g; jj += pp.ang_warps) {
           const T2* src = Pol + (int64_t)(j0 + jj) * half;
           auto ld = [&](int t) -> T2 {

@@ -317,9 +317,17 @@ fbspca_status build_host_plan(Plan& P) {
   if (S % 2 == 0) --S;                                   // odd row stride (bank spread)
   if (S > pp.ncols_x) S = pp.ncols_x | 1;
   pp.S = S;
+  // pow2 plans (n_theta = 2 M, M in {64..512}) run the ring FFTs as pairs of half-length FFTs in the per-warp
+  // FFT scratch (kernels_polar.cu K3): the staging [k][ring] for 32 rings is all the region holds then
+  const bool ring_pairs = P.n_theta == 2 * M && (M == 64 || M == 128 || M == 256 || M == 512);
+  if (ring_pairs) {
+    Gsel = std::min(32, P.n_xi);
+    while (Gsel > 2 && (Gsel | 1) * kk * csz > std::max(rows_g * S * csz, pp.fft_warps * M * csz)) Gsel /= 2;
+  }
   const int G = Gsel;
   pp.ring_group = G;
-  const int region = std::max(std::max(rows_g * S * csz, pp.fft_warps * M * csz), ang_scr + (G | 1) * kk * csz);
+  const int region = std::max(std::max(rows_g * S * csz, pp.fft_warps * M * csz),
+                              (ring_pairs ? 0 : ang_scr) + (G | 1) * kk * csz);
   pp.smem_region_bytes = region;
   {   // image staged behind the phase-0 grid rows (pow2) or the per-warp row results (runtime sizes)
     const int used = std::max(L * S, pp.fft_warps * M);            // complex elements
