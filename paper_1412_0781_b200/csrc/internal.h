@@ -42,6 +42,7 @@ struct PolarParams {
   int ring_group;                 // rings staged together in the angular pass
   int smem_region_bytes;          // bytes of the shared work region (complex units * sizeof)
   int img_off;                    // complex-element offset of the staged image in the region (-1: read global)
+  int img_prefetch;               // 1: the next image is loaded (cp.async) during the angular pass
   FftPlan fft_M, fft_theta;
   // device pointers (plan-owned)
   const void* deapod;             // L values (T): d(i) = 1/Phi(i/M), i = a - floor(L/2)

@@ -237,6 +237,17 @@ __device__ __forceinline__ void fft_any(const FftPlan& f, Ld ld, St st, T2* A, T
   else fft_rt<T2>(f, ld, st, A, B, tw, lane);
 }
 
+// ---------------------------------------------------------------- cp.async (LDGSTS): many loads in flight
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // ---------------------------------------------------------------- ES window weights
 // phi(d) = exp(beta (sqrt(1 - (d/hw)^2) - 1)), |d| <= hw.  fp32: MUFU sqrt.approx / ex2.approx
 // (relative error ~1e-7, far below the 1e-5 NUFFT budget); fp64: exact.
@@ -327,21 +338,28 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
   const Es<T> phi(pp.half_w, pp.beta);
   const int G = pp.ring_group;
 
+  // The image is staged in shared memory behind the phase-0 grid rows.  Its load is issued with cp.async right
+  // after the previous image's gather (the angular pass only touches the staging rows in front of it), so it
+  // overlaps the ring FFTs and the write-out.
+  T* simg = reinterpret_cast<T*>(region + (pp.img_off >= 0 ? pp.img_off : 0));
+  const int nel = L * L;
+  auto issue_image = [&](int64_t im) {
+    const T* src = images + im * img_stride;
+    if ((nel * (int)sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+      for (int i = tid; i < nel * (int)sizeof(T) / 16; i += nthr)
+        cp_async16(reinterpret_cast<int4*>(simg) + i, reinterpret_cast<const int4*>(src) + i);
+    } else {
+      for (int i = tid; i < nel; i += nthr) simg[i] = __ldg(src + i);
+    }
+  };
+  bool prefetched = false;
   PROF_INIT();
   for (int64_t img = blockIdx.x; img < n_img; img += gridDim.x) {
     const T* I = images + img * img_stride;
-    // ---------------- stage the image in shared memory (all threads, 16-byte loads when possible)
     const T* Isrc = I;
     if (pp.img_off >= 0) {
-      T* simg = reinterpret_cast<T*>(region + pp.img_off);
-      const int nel = L * L;
-      if ((nel * (int)sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(I) & 15) == 0) {
-        const int4* src = reinterpret_cast<const int4*>(I);
-        int4* dst = reinterpret_cast<int4*>(simg);
-        for (int i = tid; i < nel * (int)sizeof(T) / 16; i += nthr) dst[i] = __ldg(src + i);
-      } else {
-        for (int i = tid; i < nel; i += nthr) simg[i] = __ldg(I + i);
-      }
+      if (!prefetched) issue_image(img);
+      cp_async_wait_all();
       __syncthreads();
       Isrc = simg;
     }
@@ -401,8 +419,12 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         for (int a = warp; a < L; a += nwarps) {
           const T2* src = X + (int64_t)a * ncx + (lo - col_lo);
           T2* dst = Gc + (size_t)a * S;
-          for (int cc = lane; cc < ncols; cc += 32) dst[cc] = src[cc];
+          for (int cc = lane; cc < ncols; cc += 32) {
+            if constexpr (sizeof(T2) == 8) cp_async8(dst + cc, src + cc);
+            else dst[cc] = src[cc];
+          }
         }
+        cp_async_wait_all();
         __syncthreads();
       }
       PROF_MARK(1);
@@ -474,6 +496,8 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       __syncthreads();
       PROF_MARK(3);
     }
+    prefetched = false;
+    if (pp.img_prefetch && img + gridDim.x < n_img) { issue_image(img + gridDim.x); prefetched = true; }
 
     // ---------------- K3: ring FFTs, staged [k][jj], written k-major.
     // pow2 plans: ring pairs (j, j+1) per warp as two half-length (N = n_theta/2) FFTs.  With f the half ring and

@@ -333,6 +333,9 @@ fbspca_status build_host_plan(Plan& P) {
     const int used = std::max(L * S, pp.fft_warps * M);            // complex elements
     const int need = used + (L * L * (csz / 2) + csz - 1) / csz + 2;
     pp.img_off = (need * csz <= region) ? ((used + 1) & ~1) : -1;    // 16-B aligned start
+    // the angular pass uses the region below img_off only (staging [k][ring], + ping-pongs on runtime sizes)
+    const int ang_use = (ring_pairs ? 0 : ang_scr) + (G | 1) * kk * csz;
+    pp.img_prefetch = (pp.img_off >= 0 && ang_use <= pp.img_off * csz) ? 1 : 0;
   }
   P.polar_smem = fixed + region;
   // phases over columns: phase p holds m2 in [lo_p, lo_p + S) and owns nodes with b2 in [lo_p, lo_p + S - w]
