@@ -29,6 +29,21 @@ template <typename T2> __device__ __forceinline__ T2 cmul(T2 a, T2 b) {
 }
 template <typename T2> __device__ __forceinline__ T2 mul_mi(T2 a) { return {a.y, -a.x}; }   // -i * a
 
+// acc + w g for a real weight w: one packed FFMA2 (fma.rn.f32x2, w broadcast) in fp32, two FMAs in fp64
+__device__ __forceinline__ float2 rfma(float w, float2 g, float2 acc) {
+  unsigned long long r, gg, aa, ww;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(gg) : "f"(g.x), "f"(g.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(aa) : "f"(acc.x), "f"(acc.y));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(ww) : "f"(w));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(ww), "l"(gg), "l"(aa));
+  float2 o;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+  return o;
+}
+__device__ __forceinline__ double2 rfma(double w, double2 g, double2 acc) {
+  return {fma(w, g.x, acc.x), fma(w, g.y, acc.y)};
+}
+
 // ---------------------------------------------------------------- small forward DFTs (e^{-2 pi i})
 template <typename T2, int R> struct Dft;
 template <typename T2> struct Dft<T2, 2> {
@@ -447,11 +462,14 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       __syncthreads();
       PROF_MARK(2);
       const int nb = pp.phase_node_begin[ph], ne = pp.phase_node_begin[ph + 1];
+      int4 rec_next = make_int4(0, 0, 0, 0);          // fp32: next entry's record loaded one iteration ahead
+      if (sizeof(T) == 4 && nb + tid < ne) rec_next = __ldg(pp.noderec + nb + tid);
       for (int t = nb + tid; t < ne; t += nthr) {
         int j, l, b1, b2;
         T t1, t2;
         if constexpr (sizeof(T) == 4) {             // fp32: precomputed record (one 16-B load)
-          const int4 rec = __ldg(pp.noderec + t);
+          const int4 rec = rec_next;
+          if (t + nthr < ne) rec_next = __ldg(pp.noderec + t + nthr);
           b1 = int(short(rec.x & 0xFFFF)); b2 = rec.x >> 16;
           t1 = __int_as_float(rec.y); t2 = __int_as_float(rec.z);
           j = int(uint32_t(rec.w) >> 16); l = rec.w & 0xFFFF;
@@ -476,19 +494,13 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           const T2* gb = gcol + (size_t)(row0 - b1 - q) * S;        // node (-k1, k2), mirrored taps
           T2 sa = T2{T(0), T(0)}, sb = T2{T(0), T(0)};
 #pragma unroll
-          for (int c = 0; c < W; ++c) {
-            const T2 g = ga[c];
-            sa.x += wy[c] * g.x; sa.y += wy[c] * g.y;
-          }
+          for (int c = 0; c < W; ++c) sa = rfma(wy[c], ga[c], sa);
           if (pair) {
 #pragma unroll
-            for (int c = 0; c < W; ++c) {
-              const T2 g = gb[c];
-              sb.x += wy[c] * g.x; sb.y += wy[c] * g.y;
-            }
+            for (int c = 0; c < W; ++c) sb = rfma(wy[c], gb[c], sb);
           }
-          accA.x += wx[q] * sa.x; accA.y += wx[q] * sa.y;
-          accB.x += wx[q] * sb.x; accB.y += wx[q] * sb.y;
+          accA = rfma(wx[q], sa, accA);
+          accB = rfma(wx[q], sb, accB);
         }
         Pol[(int64_t)j * half + l] = accA;
         if (pair) Pol[(int64_t)j * half + (half - l)] = accB;
