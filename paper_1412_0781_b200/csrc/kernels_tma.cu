@@ -288,16 +288,19 @@ radial_tma_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constan
 }
 
 // ---------------------------------------------------------------- K5 (k >= 1)
-// Work item = (k, chunk of `chunk` images = 2 chunk columns).  Stage tile = [x_raw (b rows, TMA) ; x_lo (b rows,
+// Work item = (k, chunk of `chunk` images = 2 chunk columns).  Chunk tile = [x_raw (b rows, TMA) ; x_lo (b rows,
 // written by warps 0-3)], b = the smallest TMA box >= roundup16(p_k) (<= 128); one MMA per K step with
 // A = tile rows 0..127 (rows >= b: ignored outputs) and B = the whole tile (N = 2b):
 //   D[q][c] = sum x_raw[q] x_raw[c] (c < b),  D[q][b + c] = sum x_raw[q] x_lo[c]
 //   S[q][q'] = X[q][q'] + Y[q][q'] + Y[q'][q],  X = D[:, :b] (symmetric), Y = D[:, b:].
+// A stage holds CK consecutive K chunks whose TMA boxes are issued back to back, so each coefficient row is
+// read as CK x 128 contiguous bytes at once (the rows of block k are 2 n floats apart: DRAM page locality).
 // A drain group of `drain` images accumulates in one of two TMEM accumulators (fp32 accumulation never runs
 // longer than 2 drain = 256 terms); warps 0-3 drain it into fp32 registers, thread q keeping
 //   acc[c] = sum Y[q][c] (c > q),  X[q][q] + 2 Y[q][q] (c = q),  X[q][c] + Y[q][c] (c < q),
 // so that S[q][q'] = acc_q[q'] + acc_q'[q] (q < q'), S[q][q] = acc_q[q].  The item's S goes to scratch[chunk] as the
 // fp64 upper triangle (combined through shared memory); cov_reduce_kernel adds the chunks in fixed order.
+constexpr int K5_CK = 4;
 struct K5Args {
   int k_max, nchunk, chunk, drain, stages, rmax;
   int64_t i0, nb, ld;
@@ -313,8 +316,10 @@ __global__ void __launch_bounds__(192, 1)
 cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int CK = K5_CK;
   const int NS = args.stages;
-  const uint32_t stage_bytes = uint32_t(max(128, 2 * RR)) * ROWB;  // the M = 128 A operand reads 128 rows
+  const uint32_t tile_bytes = uint32_t(max(128, 2 * RR)) * ROWB;   // the M = 128 A operand reads 128 rows
+  const uint32_t stage_bytes = CK * tile_bytes;
   float* tr = reinterpret_cast<float*>(sm + NS * stage_bytes);      // RR x (RR + 1) epilogue transpose
   uint64_t* full = reinterpret_cast<uint64_t*>(tr + RR * (RR + 1));
   uint64_t* loready = full + NS;
@@ -336,7 +341,7 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
   const int n_items = args.k_max * args.nchunk;
-  const int kc_per_group = (2 * args.drain) / KC;
+  const int st_per_group = max(1, (2 * args.drain) / (KC * CK));   // stages per drain group
   auto item_geom = [&](int item, int& k, int& ch, int& nkc) {
     k = 1 + item / args.nchunk; ch = item - (k - 1) * args.nchunk;
     const int64_t img0 = args.i0 + int64_t(ch) * args.chunk;
@@ -353,11 +358,12 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
         const int bi = box_idx((args.p[k] + 15) & ~15);
         const int col0 = int(2 * (args.i0 + int64_t(ch) * args.chunk));
         const int row0 = int(args.coef_off[k]);
-        for (int kc = 0; kc < nkc; ++kc, ++it) {
-          const int s = it % NS;
+        for (int kc0 = 0; kc0 < nkc; kc0 += CK, ++it) {
+          const int s = it % NS, nc = min(CK, nkc - kc0);
           bar_wait(&empty[s], ((it / NS) & 1) ^ 1);
-          bar_expect_tx(&full[s], (16u << bi) * ROWB);
-          tma_2d(sm + s * stage_bytes, &tm_a.m[bi], col0 + kc * KC, row0, &full[s]);
+          bar_expect_tx(&full[s], uint32_t(nc) * (16u << bi) * ROWB);
+          for (int c = 0; c < nc; ++c)
+            tma_2d(sm + s * stage_bytes + c * tile_bytes, &tm_a.m[bi], col0 + (kc0 + c) * KC, row0, &full[s]);
         }
       }
     }
@@ -371,23 +377,26 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
         item_geom(item, k, ch, nkc);
         const int b = 16 << box_idx((args.p[k] + 15) & ~15);
         const uint32_t idesc = idesc_tf32(128, 2 * b);
-        for (int kc = 0; kc < nkc; ++kc, ++it) {
-          const bool first = (kc % kc_per_group) == 0;
-          const bool last = (kc % kc_per_group) == kc_per_group - 1 || kc == nkc - 1;
+        const int nst = (nkc + CK - 1) / CK;
+        for (int si = 0; si < nst; ++si, ++it) {
+          const bool first = (si % st_per_group) == 0;
+          const bool last = (si % st_per_group) == st_per_group - 1 || si == nst - 1;
           const int a = g & 1;
           const uint32_t d = tmem + uint32_t(a * 2 * RR);
           if (first) {
             bar_wait(&accempty[a], ((g >> 1) & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
           }
-          const int s = it % NS;
+          const int s = it % NS, nc = min(CK, nkc - si * CK);
           bar_wait(&loready[s], (it / NS) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t x = su32(sm + s * stage_bytes);
+          for (int c = 0; c < nc; ++c) {
+            const uint32_t x = su32(sm + s * stage_bytes + c * tile_bytes);
 #pragma unroll
-          for (int s4 = 0; s4 < KC / 8; ++s4) {
-            const uint32_t ko = uint32_t(s4) * 32u;
-            mma_tf32(d, desc_sw128(x + ko), desc_sw128(x + ko), idesc, (!first || s4) ? 1u : 0u);
+            for (int s4 = 0; s4 < KC / 8; ++s4) {
+              const uint32_t ko = uint32_t(s4) * 32u;
+              mma_tf32(d, desc_sw128(x + ko), desc_sw128(x + ko), idesc, (!first || c || s4) ? 1u : 0u);
+            }
           }
           mma_commit(&empty[s]);
           if (last) { mma_commit(&accfull[a]); ++g; }
@@ -404,6 +413,7 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
     item_geom(item, k, ch, nkc);
     const int pk = args.p[k];
     const int b = 16 << box_idx((pk + 15) & ~15);
+    const int nst = (nkc + CK - 1) / CK;
     float acc[RR];
 #pragma unroll
     for (int i = 0; i < RR; ++i) acc[i] = 0.f;
@@ -429,14 +439,14 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
       bar_arrive(&accempty[a]);
     };
     int pending = -1;
-    for (int kc = 0; kc < nkc; ++kc, ++it) {
-      const int s = it % NS;
+    for (int si = 0; si < nst; ++si, ++it) {
+      const int s = it % NS, nc = min(CK, nkc - si * CK);
       unsigned char* st = sm + s * stage_bytes;
       bar_wait(&full[s], (it / NS) & 1);
-      make_lo(st, st + b * ROWB, b * ROWB, tid);
+      for (int c = 0; c < nc; ++c) make_lo(st + c * tile_bytes, st + c * tile_bytes + b * ROWB, b * ROWB, tid);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       bar_arrive(&loready[s]);
-      const bool last = (kc % kc_per_group) == kc_per_group - 1 || kc == nkc - 1;
+      const bool last = (si % st_per_group) == st_per_group - 1 || si == nst - 1;
       if (last) {                                            // drain the previous group while this one runs
         if (pending >= 0) drain(pending);
         pending = g++;
@@ -451,15 +461,10 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
     }
     named_sync(1, 128);
     double* dst = args.scratch + int64_t(ch) * args.scratch_stride + args.blk_off[k];
-    const int64_t tri = int64_t(pk) * (pk + 1) / 2;
-    for (int64_t e = tid; e < tri; e += 128) {
-      // e -> (r, c), r <= c, row-major packed upper triangle
-      int r = int((2.0 * pk + 1 - sqrt((2.0 * pk + 1) * (2.0 * pk + 1) - 8.0 * double(e))) / 2);
-      while (r > 0 && int64_t(r) * pk - int64_t(r) * (r - 1) / 2 > e) --r;
-      while (int64_t(r + 1) * pk - int64_t(r + 1) * r / 2 <= e) ++r;
-      const int c = r + int(e - (int64_t(r) * pk - int64_t(r) * (r - 1) / 2));
-      const double v = r == c ? double(tr[r * (RR + 1) + r]) : double(tr[r * (RR + 1) + c]) + double(tr[c * (RR + 1) + r]);
-      dst[e] = v;
+    for (int r = warp; r < pk; r += 4) {                     // row r of the packed upper triangle: warp-wide
+      double* drow = dst + (int64_t)r * pk - (int64_t)r * (r - 1) / 2;
+      for (int c = r + lane; c < pk; c += 32)
+        drow[c - r] = c == r ? double(tr[r * (RR + 1) + r]) : double(tr[r * (RR + 1) + c]) + double(tr[c * (RR + 1) + r]);
     }
   }
   named_sync(1, 128);
@@ -532,9 +537,9 @@ cudaError_t launch_radial_tma(const Plan& P, int64_t nb, int64_t i0, int64_t ld,
 
 template <int RR>
 static cudaError_t launch_cov_tma_t(const Plan& P, const MapSet& ta, K5Args& a, cudaStream_t s) {
-  const int stage = std::max(128, 2 * RR) * ROWB;
+  const int stage = K5_CK * std::max(128, 2 * RR) * ROWB;
   const int fixed = RR * (RR + 1) * 4 + 1024 + 256;
-  a.stages = std::max(2, std::min(8, (200 * 1024 - fixed) / stage));
+  a.stages = std::max(2, std::min(8, (227 * 1024 - fixed) / stage));
   const int smem = a.stages * stage + fixed;
   static int configured = 0;
   if (configured < smem) {
