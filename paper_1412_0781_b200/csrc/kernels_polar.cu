@@ -575,8 +575,21 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       __syncthreads();
       PROF_MARK(4);
       {
-        // warp per k: lanes write rings j0 + lane (re row then im row), 128-B coalesced stores
         const int64_t kstride = pp.ghat_kstride;
+        const int kmx4 = pp.k_max;
+        if (sizeof(T) == 4 && g == 32 && (n_xi & 3) == 0) {
+          // full fp32 group: lane = (k of 4, quad of 4 rings); 16-byte stores of the re and im rows
+          const int kk = lane >> 3, qd = lane & 7;
+          T* base = ghat + img * 2 * (int64_t)n_xi + j0 + 4 * qd;
+          for (int k = warp * 4 + kk; k <= kmx4; k += nwarps * 4) {
+            const T2* sp = stg + (size_t)k * GS + 4 * qd;
+            const T2 v0 = sp[0], v1 = sp[1], v2 = sp[2], v3 = sp[3];
+            T* d = base + (int64_t)k * kstride;
+            *reinterpret_cast<float4*>(d) = make_float4(v0.x, v1.x, v2.x, v3.x);
+            *reinterpret_cast<float4*>(d + n_xi) = make_float4(v0.y, v1.y, v2.y, v3.y);
+          }
+        } else {
+        // warp per k: lanes write rings j0 + lane (re row then im row), 128-B coalesced stores
         // g <= 16: each half-warp writes one k (two k per warp instruction); else a warp per k
         const int per = g <= 16 ? 2 : 1;
         const int sub = per == 2 ? (lane >> 4) : 0, ln = per == 2 ? (lane & 15) : lane, lstep = per == 2 ? 16 : 32;
@@ -604,6 +617,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           }
           dst += 4 * (int64_t)kstep * kstride;
           sp += (size_t)4 * kstep * GS;
+        }
         }
       }
       __syncthreads();
