@@ -156,6 +156,7 @@ fbspca_status upload_plan(Plan& P) {
   FB_CUDA(upload((void**)&P.d_cs, P.cs.data(), P.cs.size()), "upload cs");
   FB_CUDA(upload((void**)&P.d_nodes, P.nodes.data(), P.nodes.size()), "upload nodes");
   FB_CUDA(upload((void**)&P.d_noderec, P.noderec.data(), P.noderec.size()), "upload node records");
+  FB_CUDA(upload((void**)&P.d_dnoderec, P.dnoderec.data(), P.dnoderec.size()), "upload double node records");
   PolarParams& pp = P.pp;
   pp.xscratch_stride = (int64_t)P.L * pp.ncols_x;
   pp.pscratch_stride = (int64_t)P.n_xi * pp.half;
@@ -181,6 +182,7 @@ fbspca_status upload_plan(Plan& P) {
   pp.deapod = P.d_deapod; pp.tw_M = P.d_tw_M; pp.tw_theta = P.d_tw_theta;
   pp.rho = P.d_rho; pp.cs = P.d_cs; pp.nodes = P.d_nodes;
   pp.noderec = reinterpret_cast<const int4*>(P.d_noderec);
+  pp.dnoderec = reinterpret_cast<const int4*>(P.d_dnoderec);
   pp.xscratch = P.d_xscratch; pp.pscratch = P.d_pscratch;
   FB_CUDA(upload((void**)&P.d_pp, &pp, 1), "upload polar params");
   return FBSPCA_OK;
@@ -192,7 +194,7 @@ void free_plan(Plan& P) {
   void* ptrs[] = {P.d_table, P.d_deapod, P.d_tw_M, P.d_tw_theta, P.d_rho, P.d_cs, P.d_nodes, P.d_xscratch,
                   P.d_pscratch, P.d_ghat, P.d_partial, P.d_p, P.d_coef_off, P.d_blk_off, P.d_evec_off,
                   P.d_eig_work, P.d_eig_sweeps, P.d_coef_k, P.d_pp, P.d_cov_scratch, P.d_cov_scratch0, P.d_table_hi, P.d_table_lo,
-                  P.d_noderec};
+                  P.d_noderec, P.d_dnoderec};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& ev : P.tevents) { cudaEventDestroy(ev.second.first); cudaEventDestroy(ev.second.second); }
   if (P.ev_fork) cudaEventDestroy(P.ev_fork);

@@ -34,6 +34,7 @@ struct PolarParams {
   int n_phase;
   int phase_lo[kMaxPhases];       // first column (m2) of phase p
   int phase_node_begin[kMaxPhases + 1];
+  int phase_dbl_begin[kMaxPhases + 1];       // double entries (2 int4 each) of phase p: [begin[p], begin[p+1])
   double beta;
   double half_w;                  // w/2
   int nwarps;                     // warps per CTA (gather, fills)
@@ -52,6 +53,7 @@ struct PolarParams {
   const double* cs;               // half x 2: cos(theta_l), sin(theta_l)
   const uint32_t* nodes;          // (j << 16) | l, grouped by phase
   const int4* noderec;            // per entry {b1 | b2 << 16, t1, t2, (j << 16) | l} (fp32 path)
+  const int4* dnoderec;           // per double entry 2 int4 (plan.cpp "Double entries")
   void* xscratch;                 // per resident CTA: L x ncols_x complex
   void* pscratch;                 // per resident CTA: n_xi x half complex
   int64_t ghat_kstride;           // ghat elements (T) per k: 2 max_batch n_xi (fixed, so one TMA map serves all batches)
@@ -85,6 +87,7 @@ struct Plan {
   PolarParams pp{};                      // host copy (device pointers filled at upload)
   std::vector<uint32_t> nodes;
   std::vector<int32_t> noderec;          // 4 per node entry
+  std::vector<int32_t> dnoderec;         // 8 per double entry
   int polar_smem = 0;
   int polar_grid = 0;                    // resident CTAs of the polar kernel
   // device buffers
@@ -99,6 +102,7 @@ struct Plan {
   double* d_cs = nullptr;
   uint32_t* d_nodes = nullptr;
   int32_t* d_noderec = nullptr;
+  int32_t* d_dnoderec = nullptr;
   PolarParams* d_pp = nullptr;           // device copy of pp
   void* d_xscratch = nullptr;
   void* d_pscratch = nullptr;

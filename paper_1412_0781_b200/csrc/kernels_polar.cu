@@ -461,6 +461,58 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       }
       __syncthreads();
       PROF_MARK(2);
+      if constexpr (sizeof(T) == 4 && W == 6 && MC > 0) {
+        // double entries: nodes a, b of one ring (+ their mirrors) over one shared 7 x 7 window at U
+        const int db = pp.phase_dbl_begin[ph], de = pp.phase_dbl_begin[ph + 1];
+        for (int t = db + tid; t < de; t += nthr) {
+          const int4 r0 = __ldg(pp.dnoderec + 2 * t), r1 = __ldg(pp.dnoderec + 2 * t + 1);
+          const int u1 = int(short(r0.x & 0xFFFF)), u2 = r0.x >> 16, of = r0.w;
+          const float t1a = __int_as_float(r0.y), t2a = __int_as_float(r0.z);
+          const float t1b = __int_as_float(r1.y), t2b = __int_as_float(r1.z);
+          float xa[7], ya[7], xb[7], yb[7];
+          {
+            float wa[6], va[6], wb[6], vb[6];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+              wa[q] = phi(t1a - float(q)); va[q] = phi(t2a - float(q));
+              wb[q] = phi(t1b - float(q)); vb[q] = phi(t2b - float(q));
+            }
+            const bool o1a = of & 1, o2a = of & 2, o1b = of & 4, o2b = of & 8;
+#pragma unroll
+            for (int r = 0; r < 7; ++r) {
+              xa[r] = o1a ? (r ? wa[r - 1] : 0.f) : (r < 6 ? wa[r] : 0.f);
+              ya[r] = o2a ? (r ? va[r - 1] : 0.f) : (r < 6 ? va[r] : 0.f);
+              xb[r] = o1b ? (r ? wb[r - 1] : 0.f) : (r < 6 ? wb[r] : 0.f);
+              yb[r] = o2b ? (r ? vb[r - 1] : 0.f) : (r < 6 ? vb[r] : 0.f);
+            }
+          }
+          const T2* gcol = Gc + (u2 - lo);
+          T2 aa = T2{0.f, 0.f}, ab = aa, ma = aa, mb = aa;      // (node a, node b) x (direct, mirrored)
+#pragma unroll
+          for (int r = 0; r < 7; ++r) {
+            const T2* ga = gcol + (size_t)(u1 + r + row0) * S;
+            const T2* gm = gcol + (size_t)(row0 - u1 - r) * S;
+            T2 sa = T2{0.f, 0.f}, sb = sa, na = sa, nb2 = sa;
+#pragma unroll
+            for (int c = 0; c < 7; ++c) {
+              const T2 g = ga[c];
+              sa = rfma(ya[c], g, sa); sb = rfma(yb[c], g, sb);
+            }
+#pragma unroll
+            for (int c = 0; c < 7; ++c) {
+              const T2 g = gm[c];
+              na = rfma(ya[c], g, na); nb2 = rfma(yb[c], g, nb2);
+            }
+            aa = rfma(xa[r], sa, aa); ab = rfma(xb[r], sb, ab);
+            ma = rfma(xa[r], na, ma); mb = rfma(xb[r], nb2, mb);
+          }
+          const int ja = int(uint32_t(r1.x) >> 16), la = r1.x & 0xFFFF, jb = int(uint32_t(r1.w) >> 16), lb = r1.w & 0xFFFF;
+          Pol[(int64_t)ja * half + la] = aa;
+          Pol[(int64_t)ja * half + (half - la)] = ma;
+          Pol[(int64_t)jb * half + lb] = ab;
+          Pol[(int64_t)jb * half + (half - lb)] = mb;
+        }
+      }
       const int nb = pp.phase_node_begin[ph], ne = pp.phase_node_begin[ph + 1];
       int4 rec_next = make_int4(0, 0, 0, 0);          // fp32: next entry's record loaded one iteration ahead
       if (sizeof(T) == 4 && nb + tid < ne) rec_next = __ldg(pp.noderec + nb + tid);

@@ -4,6 +4,7 @@
 // Newton, Gauss-Legendre by Newton on the Legendre recurrence, and the NUFFT window/deapodisation
 // are product-only (the oracle uses a direct Fourier sum).
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -119,6 +120,8 @@ int ceil_guard(double x) { return int(std::ceil(x - 1e-9)); }   // reading Q4
 // full (16) except the phase's last.
 
 // Model cost (wavefronts per tap, summed over warps) of a node order under the bank model above.
+std::vector<uint32_t> pack_gather_items(const std::vector<std::array<int, 3>>& items, int S);
+
 long gather_bank_cost(const std::vector<uint32_t>& ord, const std::vector<double>& rho, const std::vector<double>& cs,
                       double hw, int S, int half, int group = 32) {
   long tot = 0;
@@ -142,28 +145,20 @@ long gather_bank_cost(const std::vector<uint32_t>& ord, const std::vector<double
   return tot;
 }
 
-std::vector<uint32_t> pack_gather_warps(const std::vector<uint32_t>& nodes, const std::vector<double>& rho,
-                                        const std::vector<double>& cs, double hw, int S) {
+std::vector<uint32_t> pack_gather_items(const std::vector<std::array<int, 3>>& items, int S) {
   struct Anc { int b1, b2; std::vector<uint32_t> ids; };
   std::vector<Anc> anc;
   {
-    std::vector<std::pair<std::pair<int, int>, uint32_t>> keyed;
-    keyed.reserve(nodes.size());
-    for (uint32_t nd : nodes) {
-      const int j = int(nd >> 16), l = int(nd & 0xffffu);
-      const double k1 = rho[j] * cs[2 * l], k2 = rho[j] * cs[2 * l + 1];
-      keyed.push_back({{int(std::ceil(k1 - hw)), int(std::ceil(k2 - hw))}, nd});
-    }
+    std::vector<std::array<int, 3>> keyed = items;
     std::sort(keyed.begin(), keyed.end());
     for (auto& e : keyed) {
-      if (anc.empty() || anc.back().b1 != e.first.first || anc.back().b2 != e.first.second)
-        anc.push_back({e.first.first, e.first.second, {}});
-      anc.back().ids.push_back(e.second);
+      if (anc.empty() || anc.back().b1 != e[0] || anc.back().b2 != e[1]) anc.push_back({e[0], e[1], {}});
+      anc.back().ids.push_back(uint32_t(e[2]));
     }
   }
   auto cls = [&](int b1, int b2, int sgn) { return (((sgn * b1 * S + b2) % 16) + 16) % 16; };
   std::vector<uint32_t> out;
-  out.reserve(nodes.size());
+  out.reserve(items.size());
   std::vector<char> used(anc.size(), 0);
   std::vector<size_t> done_ids(anc.size(), 0);
   size_t next = 0, left = anc.size();
@@ -338,45 +333,80 @@ fbspca_status build_host_plan(Plan& P) {
     pp.img_prefetch = (pp.img_off >= 0 && ang_use <= pp.img_off * csz) ? 1 : 0;
   }
   P.polar_smem = fixed + region;
-  // phases over columns: phase p holds m2 in [lo_p, lo_p + S) and owns nodes with b2 in [lo_p, lo_p + S - w]
-  std::vector<int> order(b2.size());
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return b2[a] < b2[b]; });
-  P.nodes.clear();
-  int np = 0, lo = b2min;
-  size_t pos = 0;
-  while (pos < order.size()) {
-    if (np >= kMaxPhases) { set_error("too many column phases"); return FBSPCA_ERR_CONFIG; }
-    pp.phase_lo[np] = lo;
-    pp.phase_node_begin[np] = int(P.nodes.size());
-    std::vector<uint32_t> ph;
-    while (pos < order.size() && b2[order[pos]] <= lo + S - w) {
-      int id = order[pos++];
-      int j = id / half, l = id % half;
-      // pair leaders only: node (j, half - l) = (-k1, k2) is gathered with (j, l) (same columns)
-      if (2 * l <= half) ph.push_back((uint32_t(j) << 16) | uint32_t(l));
-    }
-    {
-      std::vector<uint32_t> packed = pack_gather_warps(ph, rho, cs, hw, S);
-      if (getenv("FBSPCA_DEBUG_PLAN")) {
-        std::vector<uint32_t> srt = ph;
-        auto key = [&](uint32_t nd) {
-          const int j = int(nd >> 16), l = int(nd & 0xffffu);
-          return std::make_pair(int(std::ceil(rho[j] * cs[2 * l] - hw)), int(std::ceil(rho[j] * cs[2 * l + 1] - hw)));
-        };
-        std::stable_sort(srt.begin(), srt.end(), [&](uint32_t x, uint32_t y) { return key(x) < key(y); });
-        fprintf(stderr, "phase %d: %zu pairs, half-warp bank model wavefronts/tap: (b1,b2)-sorted %ld, packed %ld, "
-                "floor %zu\n", np, ph.size(), gather_bank_cost(srt, rho, cs, hw, S, half, 16),
-                gather_bank_cost(packed, rho, cs, hw, S, half, 16), 2 * ((ph.size() + 15) / 16));
+  // phases over columns: phase p holds m2 in [lo_p, lo_p + S) and owns single entries with b2 in
+  // [lo_p, lo_p + S - w] and double entries with union anchor U2 in [lo_p, lo_p + S - w - 1].
+  //
+  // Double entries (fp32 W = 6 pow2 kernels): two pair leaders (j, l), (j, l + 1) of one ring whose anchors differ
+  // by at most 1 in each direction share a (w + 1) x (w + 1) window at U = min(b): 49 + 49 grid loads for four
+  // nodes instead of 4 x 36 (the mirrored pair members (j, half - l), (j, half - l - 1) share it mirrored).
+  auto anchor = [&](int j, int l) {
+    return std::make_pair(int(std::ceil(rho[j] * cs[2 * l] - hw)), int(std::ceil(rho[j] * cs[2 * l + 1] - hw)));
+  };
+  std::vector<int> phase_lo;
+  for (int lo = b2min; lo <= b2max; lo += S - w + 1) phase_lo.push_back(lo);
+  if ((int)phase_lo.size() > kMaxPhases) { set_error("too many column phases"); return FBSPCA_ERR_CONFIG; }
+  auto phase_of_single = [&](int b2) { return std::min<int>((b2 - b2min) / (S - w + 1), (int)phase_lo.size() - 1); };
+  auto phase_of_double = [&](int u2) {     // all w + 1 columns must be valid grid columns of the phase
+    const int p = (u2 - b2min) / (S - w + 1);
+    if (p >= (int)phase_lo.size()) return -1;
+    const int last = std::min(phase_lo[p] + S - 1, b2max + w - 1);
+    return (u2 + w <= last) ? p : -1;
+  };
+  const bool doubles = P.dt == FBSPCA_F32 && w == 6 && ring_pairs && !getenv("FBSPCA_NO_DOUBLES");
+  std::vector<std::vector<std::array<int, 3>>> ph_single(phase_lo.size()), ph_double(phase_lo.size());
+  std::vector<uint32_t> singles;
+  std::vector<std::array<uint32_t, 2>> dbl;
+  for (int j = 0; j < P.n_xi; ++j) {
+    for (int l = 0; 2 * l <= half; ++l) {
+      const auto a = anchor(j, l);
+      if (doubles && l >= 1 && 2 * (l + 1) < half) {
+        const auto b = anchor(j, l + 1);
+        const int u1 = std::min(a.first, b.first), u2 = std::min(a.second, b.second);
+        const int p = phase_of_double(u2);
+        if (std::abs(a.first - b.first) <= 1 && std::abs(a.second - b.second) <= 1 && p >= 0) {
+          ph_double[p].push_back({u1, u2, int(dbl.size())});
+          dbl.push_back({(uint32_t(j) << 16) | uint32_t(l), (uint32_t(j) << 16) | uint32_t(l + 1)});
+          ++l;
+          continue;
+        }
       }
-      ph.swap(packed);
+      ph_single[phase_of_single(a.second)].push_back({a.first, a.second, int(singles.size())});
+      singles.push_back((uint32_t(j) << 16) | uint32_t(l));
     }
-    P.nodes.insert(P.nodes.end(), ph.begin(), ph.end());
+  }
+  P.nodes.clear();
+  P.dnoderec.clear();
+  int np = 0;
+  for (size_t p = 0; p < phase_lo.size(); ++p) {
+    pp.phase_lo[np] = phase_lo[p];
+    pp.phase_node_begin[np] = int(P.nodes.size());
+    pp.phase_dbl_begin[np] = int(P.dnoderec.size() / 8);
+    for (uint32_t id : pack_gather_items(ph_single[p], S)) P.nodes.push_back(singles[id]);
+    for (uint32_t id : pack_gather_items(ph_double[p], S)) {
+      // {U1 | U2 << 16, t1a, t2a, offsets}, {node a, t1b, t2b, node b}; t = k - b of each node's own anchor
+      int32_t rec[8];
+      const uint32_t na = dbl[id][0], nb = dbl[id][1];
+      const int ja = int(na >> 16), la = int(na & 0xffffu), jb = int(nb >> 16), lb = int(nb & 0xffffu);
+      const auto aa = anchor(ja, la), ab = anchor(jb, lb);
+      const int u1 = std::min(aa.first, ab.first), u2 = std::min(aa.second, ab.second);
+      const float t1a = float(rho[ja] * cs[2 * la] - aa.first), t2a = float(rho[ja] * cs[2 * la + 1] - aa.second);
+      const float t1b = float(rho[jb] * cs[2 * lb] - ab.first), t2b = float(rho[jb] * cs[2 * lb + 1] - ab.second);
+      rec[0] = int32_t((uint32_t(u1) & 0xFFFFu) | (uint32_t(u2) << 16));
+      std::memcpy(&rec[1], &t1a, 4); std::memcpy(&rec[2], &t2a, 4);
+      rec[3] = (aa.first - u1) | ((aa.second - u2) << 1) | ((ab.first - u1) << 2) | ((ab.second - u2) << 3);
+      rec[4] = int32_t(na);
+      std::memcpy(&rec[5], &t1b, 4); std::memcpy(&rec[6], &t2b, 4);
+      rec[7] = int32_t(nb);
+      P.dnoderec.insert(P.dnoderec.end(), rec, rec + 8);
+    }
+    if (getenv("FBSPCA_DEBUG_PLAN"))
+      fprintf(stderr, "phase %d: lo %d, %zu single pair-leaders, %zu doubles\n", np, phase_lo[p], ph_single[p].size(),
+              ph_double[p].size());
     ++np;
-    lo = lo + S - w + 1;
   }
   pp.n_phase = np;
   pp.phase_node_begin[np] = int(P.nodes.size());
+  pp.phase_dbl_begin[np] = int(P.dnoderec.size() / 8);
   P.rho = rho;
   P.cs = cs;
   // per-entry record for the fp32 gather: {b1 | b2 << 16, t1, t2, (j << 16) | l}, the same fp64 arithmetic
