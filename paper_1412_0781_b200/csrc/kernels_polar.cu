@@ -560,8 +560,10 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       __syncthreads();
       PROF_MARK(3);
     }
+    // the next image's load is issued after the first ring group's FFTs (so it does not queue in front of the
+    // polar-sample loads of group 0)
     prefetched = false;
-    if (pp.img_prefetch && img + gridDim.x < n_img) { issue_image(img + gridDim.x); prefetched = true; }
+    const bool want_prefetch = pp.img_prefetch && img + gridDim.x < n_img;
 
     // ---------------- K3: ring FFTs, staged [k][jj], written k-major.
     // pow2 plans: ring pairs (j, j+1) per warp as two half-length (N = n_theta/2) FFTs.  With f the half ring and
@@ -572,9 +574,82 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
     // Runtime sizes: one full n_theta-point FFT per ring rebuilt from the half ring.
     T2* stg = (MC > 0) ? region : region + (size_t)pp.ang_warps * 2 * NTP;
     const int GS = G | 1;                            // odd staging stride (bank spread)
+    // MC = 256 (one ring pair per warp per group): the pair's first-stage inputs f[lane + 32 r], r < 8, of both
+    // rings are loaded into registers one group ahead (the loads of group j0 + G fly during group j0's FFTs and
+    // write-out), and feed both the U and the V transform -- one L2 read of the polar samples, latency hidden.
+    constexpr bool REGPF = (MC == 256) && sizeof(T) == 4;
+    T2 pfa[REGPF ? 8 : 1], pfb[REGPF ? 8 : 1];
+    const bool regpf = REGPF && G <= 2 * pp.fft_warps;
+    auto load_pair = [&](int jg) {
+      if constexpr (REGPF) {
+        const int jj = 2 * warp, gg = min(G, n_xi - jg);
+        if (jg < n_xi && warp < pp.fft_warps && jj < gg) {
+          const T2* fa = Pol + (int64_t)(jg + jj) * half;
+          const bool two = jj + 1 < gg;
+          // volatile: issued here (not sunk to the use a group later), completion tracked by the scoreboard
+          const T2* fb = two ? fa + half : fa;
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            asm volatile("ld.global.v2.f32 {%0, %1}, [%2];" : "=f"(pfa[r].x), "=f"(pfa[r].y) : "l"(fa + lane + 32 * r));
+            asm volatile("ld.global.v2.f32 {%0, %1}, [%2];" : "=f"(pfb[r].x), "=f"(pfb[r].y) : "l"(fb + lane + 32 * r));
+          }
+          if (!two) {
+#pragma unroll
+            for (int r = 0; r < 8; ++r) pfb[r] = T2{T(0), T(0)};
+          }
+        }
+      }
+    };
+    if (regpf) load_pair(0);
     for (int j0 = 0; j0 < n_xi; j0 += G) {
       const int g = min(G, n_xi - j0);
-      if constexpr (MC > 0) {
+      bool done_reg = false;
+      if constexpr (REGPF) if (regpf) {
+        done_reg = true;
+        const int kmx = pp.k_max;
+        T2* res = fft_result_in_A<MC>() ? myA : myB;
+        auto stR = [res](int i, T2 v) { res[padi(i)] = v; };
+        const int jj = 2 * warp;
+        if (warp < pp.fft_warps && jj < g) {
+          const bool two = jj + 1 < g;
+          T2 ca[REGPF ? 8 : 1], cb[REGPF ? 8 : 1];
+#pragma unroll
+          for (int r = 0; r < (REGPF ? 8 : 1); ++r) { ca[r] = pfa[r]; cb[r] = pfb[r]; }
+          load_pair(j0 + G);                          // next group's inputs, consumed one iteration later
+          // stage-1 index t = lane + 32 r  ->  r = (t - lane) >> 5 (compile-time after unrolling)
+          auto ldu = [&](int t) -> T2 { const int r = (t - lane) >> 5; return T2{ca[r].x, cb[r].x}; };
+          fft_pow2<T2, MC>(ldu, stR, myA, myB, twM, lane);
+          __syncwarp();
+          for (int m = lane; 2 * m <= kmx; m += 32) {
+            const T2 u = res[padi(m)];
+            T2 uc = res[padi((MC - m) & (MC - 1))];
+            uc.y = -uc.y;
+            const T2 sp = cadd(u, uc), dm = csub(u, uc);
+            stg[(size_t)(2 * m) * GS + jj] = sp;
+            if (two) stg[(size_t)(2 * m) * GS + jj + 1] = T2{dm.y, -dm.x};
+          }
+          __syncwarp();
+          PROF_MARK(6);
+          auto ldv = [&](int t) -> T2 {
+            const int r = (t - lane) >> 5;
+            return cmul(T2{ca[r].y, cb[r].y}, twT[t]);
+          };
+          fft_pow2<T2, MC>(ldv, stR, myA, myB, twM, lane);
+          __syncwarp();
+          for (int m = lane; 2 * m + 1 <= kmx; m += 32) {
+            const T2 v = res[padi(m)];
+            T2 vc = res[padi(MC - 1 - m)];
+            vc.y = -vc.y;
+            const T2 sp = cadd(v, vc), dm = csub(v, vc);
+            stg[(size_t)(2 * m + 1) * GS + jj] = T2{-sp.y, sp.x};
+            if (two) stg[(size_t)(2 * m + 1) * GS + jj + 1] = dm;
+          }
+          __syncwarp();
+          PROF_MARK(7);
+        }
+      }
+      if (done_reg) {
+      } else if constexpr (MC > 0) {
         const int kmx = pp.k_max;
         T2* res = fft_result_in_A<MC>() ? myA : myB;
         auto stR = [res](int i, T2 v) { res[padi(i)] = v; };
@@ -624,6 +699,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           fft_any<T2, NC>(pp.fft_theta, ld, st, angA, angB, twT, lane);
         }
       }
+      if (j0 == 0 && want_prefetch) { issue_image(img + gridDim.x); prefetched = true; }
       __syncthreads();
       PROF_MARK(4);
       {

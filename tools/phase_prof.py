@@ -47,7 +47,7 @@ def main():
     torch.cuda.synchronize()
     buf = (ctypes.c_ulonglong * (148 * 8))()
     LB.lib().fbspca_debug_phase_prof(buf, 148 * 8)
-    names = ["rowpass", "fill", "colfft", "gather", "angfft", "write", "-", "-"]
+    names = ["rowpass", "fill", "colfft", "gather", "ang-wait", "write", "ang-U", "ang-V"]
     per = [sum(buf[b * 8 + i] for b in range(148)) / a.n for i in range(8)]
     tot = sum(per)
     for nm, v in zip(names, per):
