@@ -174,12 +174,20 @@ __global__ void cov_reduce_kernel(const double* __restrict__ scratch, int64_t st
   const int64_t stride0 = blk1 + (total - s0_at);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     double s = partial[i];
-    if (nsub0 > 0 && (i < blk1 || i >= s0_at)) {
-      const int64_t j = i < blk1 ? i : blk1 + (i - s0_at);
-      for (int c = 0; c < nsub0; ++c) s += scratch0[(int64_t)c * stride0 + j];
-    } else {
-      for (int c = 0; c < nchunk; ++c) s += scratch[(int64_t)c * stride + i];
+    // loads in groups of 8 issued before the (fixed-order) adds: memory-level parallelism, same rounding
+    const bool k0 = nsub0 > 0 && (i < blk1 || i >= s0_at);
+    const double* src = k0 ? scratch0 + (i < blk1 ? i : blk1 + (i - s0_at)) : scratch + i;
+    const int64_t st = k0 ? stride0 : stride;
+    const int nc = k0 ? nsub0 : nchunk;
+    int c = 0;
+    for (; c + 8 <= nc; c += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = src[(int64_t)(c + u) * st];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
     }
+    for (; c < nc; ++c) s += src[(int64_t)c * st];
     partial[i] = s;
   }
 }

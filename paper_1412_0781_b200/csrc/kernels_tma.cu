@@ -86,6 +86,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __device__ __forceinline__ float4 lo_part(float4 x) {
@@ -422,16 +430,23 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
       bar_wait(&accfull[a], (gg >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t tb = tmem + (uint32_t(32 * warp) << 16) + uint32_t(a * 2 * RR);
+      // 32 columns of X and Y in flight per wait (b is a power of two >= 16)
 #pragma unroll
-      for (int c0 = 0; c0 < RR; c0 += 16) {
-        if (c0 < b) {
-          float xv[16], yv[16];
-          tmem_ld16(tb + uint32_t(c0), xv);
-          tmem_ld16(tb + uint32_t(b + c0), yv);
+      for (int c1 = 0; c1 < RR; c1 += 32) {
+        if (c1 < b) {
+          uint32_t xr[32], yr[32];
+          const bool two = c1 + 16 < b;
+          tmem_ld16_nowait(tb + uint32_t(c1), xr);
+          tmem_ld16_nowait(tb + uint32_t(b + c1), yr);
+          if (two) { tmem_ld16_nowait(tb + uint32_t(c1 + 16), xr + 16); tmem_ld16_nowait(tb + uint32_t(b + c1 + 16), yr + 16); }
+          tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int c = c0 + i;
-            acc[c] += c > q ? yv[i] : c == q ? xv[i] + 2.f * yv[i] : xv[i] + yv[i];
+          for (int i = 0; i < 32; ++i) {
+            const int c = c1 + i;
+            if (i < 16 || two) {
+              const float xv = __uint_as_float(xr[i]), yv = __uint_as_float(yr[i]);
+              acc[c] += c > q ? yv : c == q ? xv + 2.f * yv : xv + yv;
+            }
           }
         }
       }
