@@ -262,6 +262,13 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
                "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// Drop dead scratch lines from L2 without a write-back (the per-CTA X / Pol scratch is consumed once).
+__device__ __forceinline__ void l2_discard(const void* base, size_t bytes, int tid, int nthr) {
+  const uintptr_t a0 = (reinterpret_cast<uintptr_t>(base) + 127) & ~uintptr_t(127);
+  const uintptr_t a1 = (reinterpret_cast<uintptr_t>(base) + bytes) & ~uintptr_t(127);
+  for (uintptr_t a = a0 + uintptr_t(tid) * 128; a < a1; a += uintptr_t(nthr) * 128)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+}
 
 // ---------------------------------------------------------------- ES window weights
 // phi(d) = exp(beta (sqrt(1 - (d/hw)^2) - 1)), |d| <= hw.  fp32: MUFU sqrt.approx / ex2.approx
@@ -441,6 +448,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         }
         cp_async_wait_all();
         __syncthreads();
+        if (ph == pp.n_phase - 1) l2_discard(X, (size_t)L * ncx * sizeof(T2), tid, nthr);
       }
       PROF_MARK(1);
       if (warp < pp.fft_warps) {
@@ -701,6 +709,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       }
       if (j0 == 0 && want_prefetch) { issue_image(img + gridDim.x); prefetched = true; }
       __syncthreads();
+      l2_discard(Pol + (int64_t)j0 * half, (size_t)g * half * sizeof(T2), tid, nthr);   // rings j0.. consumed
       PROF_MARK(4);
       {
         const int64_t kstride = pp.ghat_kstride;
@@ -713,8 +722,8 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             const T2* sp = stg + (size_t)k * GS + 4 * qd;
             const T2 v0 = sp[0], v1 = sp[1], v2 = sp[2], v3 = sp[3];
             T* d = base + (int64_t)k * kstride;
-            *reinterpret_cast<float4*>(d) = make_float4(v0.x, v1.x, v2.x, v3.x);
-            *reinterpret_cast<float4*>(d + n_xi) = make_float4(v0.y, v1.y, v2.y, v3.y);
+            __stcs(reinterpret_cast<float4*>(d), make_float4(v0.x, v1.x, v2.x, v3.x));        // streamed: read
+            __stcs(reinterpret_cast<float4*>(d + n_xi), make_float4(v0.y, v1.y, v2.y, v3.y)); // back by K4 only
           }
         } else {
         // warp per k: lanes write rings j0 + lane (re row then im row), 128-B coalesced stores

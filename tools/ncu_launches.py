@@ -5,10 +5,15 @@ import sys
 from collections import defaultdict
 
 
+OURS = ("polar_kernel", "radial_tma_kernel", "radial_kernel", "cov_tma_kernel", "cov_k0_kernel", "cov_reduce_kernel",
+        "cov_finalize_kernel", "cov_accum_kernel", "eig_kernel", "project_kernel")
+
+
 def short(name: str) -> str:
-    m = re.search(r"fbspca::(\w+)", name)
-    if m:
-        return "fbspca::" + m.group(1)
+    for o in OURS:
+        if o in name:
+            m = re.search(o + r"(<[^>]*>)?", name)
+            return "fbspca::" + (m.group(0) if m else o)
     return "torch/other: " + name.split("(")[0][-60:]
 
 
