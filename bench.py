@@ -309,9 +309,9 @@ def main():
         sm_max = pk.get("sm_max_mhz", 1965.0)
         alu_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12          # fp32 FFMA TFLOP/s at max clock
         achieved = wk["polar_flops"] * imgs_per_launch / (per_launch_polar_ms / 1e3) / 1e12
-        # per step: (polar + radial) per 4096-image expand batch; (k=0 fp64 SYRK + tcgen05 SYRK + chunk
-        # reduction) per 8192-image covariance batch; finalize.  NCCL's all-reduce kernel is not ours.
-        n_cov_launch = 3 * math.ceil(n_local / 8192)
+        # per step: (polar + radial) per expand batch; (tcgen05 SYRK, k=0 fp64 on the side stream, chunk
+        # reduction) per 16384-image covariance batch; finalize.  NCCL's all-reduce kernel is not ours.
+        n_cov_launch = 3 * math.ceil(n_local / 16384)
         gpu_launches = args.steps * (2 * math.ceil(n_local / plan_batch(plan)) + n_cov_launch + 1)
         kernels = {}
         for name, tms in kms.items():
@@ -324,11 +324,20 @@ def main():
             elif name == "radial_K4":
                 d["tflops"] = wk["k4"] * n_local / (tms / 1e3) / 1e12
                 d["alg_gbs"] = wk["radial_bytes"] * n_local / (tms / 1e3) / 1e9
+                d["hbm_frac"] = d["alg_gbs"] / hbm
             elif name == "cov_K5":
                 d["tflops"] = wk["k5"] * n_local / (tms / 1e3) / 1e12
                 d["alg_gbs"] = wk["cov_bytes"] * n_local / (tms / 1e3) / 1e9
+                d["hbm_frac"] = d["alg_gbs"] / hbm
             kernels[name] = d
         staged = 1.57e6 if cfg["name"] == "C3" else None
+        traffic = None                       # DRAM bytes per polar launch, from the committed ncu capture
+        try:
+            tj = json.load(open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")))
+            if cfg["name"] == "C3":
+                traffic = tj["kernels"]["polar_K1K2K3"]["dram_bytes_per_image"] * imgs_per_launch
+        except Exception:
+            traffic = None
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
@@ -338,7 +347,9 @@ def main():
                        "n_per_rank": n_local, "eps": 1e-5, "M": plan.M, "w": plan.w,
                        "l2": "inputs larger than L2 (6.5 GB images per step at C3)"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
-                         "frac": achieved / alu_peak, "traffic": None, "kernel": "polar_K1K2K3",
+                         "frac": achieved / alu_peak, "traffic": traffic, "kernel": "polar_K1K2K3",
+                         "traffic_source": "profiles/r1_ncu_traffic.json (ncu dram bytes per image x images per launch)",
+                         "algorithmic_bytes_per_launch": wk["polar_bytes"] * imgs_per_launch,
                          "peak_source": f"148 SM x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz (guide unit counts, "
                                         "MEASURED_PEAKS sm_max_mhz)",
                          "per_image_flops": wk["polar_flops"]},
