@@ -103,10 +103,15 @@ __device__ __forceinline__ float4 lo_part(float4 x) {
 
 // lo tile of `bytes` bytes (multiple of 2048), 128 threads, 16-B granules (layout-agnostic: elementwise)
 __device__ __forceinline__ void make_lo(const unsigned char* src, unsigned char* dst, int bytes, int tid) {
-  const float4* s = reinterpret_cast<const float4*>(src);
-  float4* d = reinterpret_cast<float4*>(dst);
+  const uint32_t s = su32(src), d = su32(dst);
   const int n = bytes >> 4;
-  for (int i = tid; i < n; i += 128) d[i] = lo_part(s[i]);
+#pragma unroll 4
+  for (int i = tid; i < n; i += 128) {
+    float4 x;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(s + 16 * i));
+    x = lo_part(x);
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(d + 16 * i), "f"(x.x), "f"(x.y), "f"(x.z), "f"(x.w) : "memory");
+  }
 }
 
 __device__ __forceinline__ uint32_t idesc_tf32(int M, int N) {
@@ -151,7 +156,8 @@ __global__ void __launch_bounds__(320, 1)
 radial_tma_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ MapSet tm_bh,
                   const __grid_constant__ MapSet tm_bl, const K4Args args) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned base by pointer arithmetic on the shared array (keeps the shared address space for the compiler)
+  unsigned char* sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u);
   const int NS = args.stages;
   const uint32_t a_bytes = 128 * ROWB, b_bytes = uint32_t(args.bmax) * ROWB;
   const uint32_t stage_bytes = a_bytes + 2 * b_bytes;               // A, T_hi, T_lo
@@ -323,7 +329,8 @@ template <int RR>   // register accumulators per thread (= largest box b of k >=
 __global__ void __launch_bounds__(192, 1)
 cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned base by pointer arithmetic on the shared array (keeps the shared address space for the compiler)
+  unsigned char* sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u);
   constexpr int CK = K5_CK;
   const int NS = args.stages;
   const uint32_t tile_bytes = uint32_t(max(128, 2 * RR)) * ROWB;   // the M = 128 A operand reads 128 rows

@@ -63,6 +63,8 @@ def main(rep, binary, func, src, units=1, top=45, kname=None):
                                    "L1 Wavefronts Shared", "L1 Wavefronts Shared Ideal")}
     base = int(data[0][col["Address"]], 16)
     acc = defaultdict(lambda: [0, 0, 0, 0])
+    reasons = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
+    why = defaultdict(lambda: defaultdict(int))
     f = lambda x: int(x.replace(",", "") or 0)
     for r in data:
         if len(r) < len(h):
@@ -71,6 +73,8 @@ def main(rep, binary, func, src, units=1, top=45, kname=None):
         a = acc[key]
         a[0] += f(r[col["Warp Stall Sampling (All Samples)"]]); a[1] += f(r[col["Instructions Executed"]])
         a[2] += f(r[col["L1 Wavefronts Shared"]]); a[3] += f(r[col["L1 Wavefronts Shared Ideal"]])
+        for rc in reasons:
+            why[key][rc] += f(r[h.index(rc)])
     srcl = open(src).read().split("\n")
     T = sum(a[0] for a in acc.values()) or 1
     W = sum(a[2] for a in acc.values())
@@ -80,7 +84,9 @@ def main(rep, binary, func, src, units=1, top=45, kname=None):
         a = acc[key]
         fn, l = key
         s = srcl[l - 1].strip()[:64] if fn == os.path.basename(src) and 0 < l <= len(srcl) else fn
-        print(f"{l:5d} st {100 * a[0] / T:5.1f}% wf {a[2] / units:9.0f} (ideal {a[3] / units:8.0f}) ins {a[1] / units:8.0f}  {s}")
+        top = sorted(why[key].items(), key=lambda x: -x[1])[:2]
+        tops = " ".join(f"{k[6:]}:{100 * v / max(1, a[0]):.0f}%" for k, v in top if v)
+        print(f"{l:5d} st {100 * a[0] / T:5.1f}% wf {a[2] / units:9.0f} (ideal {a[3] / units:8.0f}) ins {a[1] / units:8.0f}  [{tops}] {s}")
 
 
 if __name__ == "__main__":
