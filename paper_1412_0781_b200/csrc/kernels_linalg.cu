@@ -300,7 +300,7 @@ eig_kernel(const double* __restrict__ blocks, const int* __restrict__ p, const i
     red[tid] = dg; __syncthreads();
     for (int st = nthr / 2; st > 0; st >>= 1) { if (tid < st) red[tid] += red[tid + st]; __syncthreads(); }
     dg = red[0]; __syncthreads();
-    if (off <= 1e-30 * dg || off == 0.0) break;
+    if (off <= 1e-26 * dg || off == 0.0) break;         // off-diagonal Frobenius <= 1e-13 of the diagonal
     for (int round = 0; round < np - 1; ++round) {
       for (int i = tid; i < npairs; i += nthr) {
         auto pos = [&](int t) { return t == 0 ? 0 : 1 + (t - 1 + round) % (np - 1); };

@@ -316,7 +316,7 @@ radial_tma_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constan
 // fp64 upper triangle (combined through shared memory); cov_reduce_kernel adds the chunks in fixed order.
 constexpr int K5_CK = 4;
 struct K5Args {
-  int k_max, nchunk, chunk, drain, stages, rmax;
+  int k_max, nchunk, chunk, drain, stages, rmax, ck;              // ck: K chunks per stage (<= K5_CK)
   int64_t i0, nb, ld;
   const int* p;
   const int64_t* coef_off;
@@ -331,7 +331,7 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   // 1024-B aligned base by pointer arithmetic on the shared array (keeps the shared address space for the compiler)
   unsigned char* sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u);
-  constexpr int CK = K5_CK;
+  const int CK = args.ck;
   const int NS = args.stages;
   const uint32_t tile_bytes = uint32_t(max(128, 2 * RR)) * ROWB;   // the M = 128 A operand reads 128 rows
   const uint32_t stage_bytes = CK * tile_bytes;
@@ -559,8 +559,10 @@ cudaError_t launch_radial_tma(const Plan& P, int64_t nb, int64_t i0, int64_t ld,
 
 template <int RR>
 static cudaError_t launch_cov_tma_t(const Plan& P, const MapSet& ta, K5Args& a, cudaStream_t s) {
-  const int stage = K5_CK * std::max(128, 2 * RR) * ROWB;
   const int fixed = RR * (RR + 1) * 4 + 1024 + 256;
+  a.ck = K5_CK;                                            // fewer chunks per stage when a tile is 32 KB
+  while (a.ck > 1 && 3 * a.ck * std::max(128, 2 * RR) * ROWB > 227 * 1024 - fixed) a.ck /= 2;
+  const int stage = a.ck * std::max(128, 2 * RR) * ROWB;
   a.stages = std::max(2, std::min(8, (227 * 1024 - fixed) / stage));
   const int smem = a.stages * stage + fixed;
   static int configured = 0;

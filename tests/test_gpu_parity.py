@@ -254,3 +254,64 @@ def test_c3_full_size_sampled_parity():
     k = 5
     Ak = coeffs[plan.coef_off[k]:plan.coef_off[k + 1]]
     assert abs(np.trace(tr[k]) - (Ak.abs() ** 2).double().sum().item() / n) <= 1e-5 * np.trace(tr[k])
+
+
+def _oracle_cov_from_gpu_coeffs(coeffs, basis, chunk=8192):
+    """fp64 oracle K5 (O.covariance_partials per chunk, O.finalize_covariance) on the GPU's coefficients."""
+    n = coeffs.shape[1]
+    S = s0 = None
+    for c0 in range(0, n, chunk):
+        A = O.from_flat(coeffs[:, c0:c0 + chunk].cpu().numpy().astype(np.complex128), basis)
+        Sc, s0c, _ = O.covariance_partials(A)
+        S = Sc if S is None else [a + b for a, b in zip(S, Sc)]
+        s0 = s0c if s0 is None else s0 + s0c
+    return O.finalize_covariance(S, s0, n)
+
+
+def _spectral_checks(plan, blocks, mean, evals, evecs, m_o, C_o, tol_c=1e-4):
+    lam_o, U_o = O.block_eig(C_o)
+    C_g = F.unpack_blocks(plan, blocks.cpu().numpy())
+    scale = max(np.abs(c).max() for c in C_o)
+    err_c = max(np.abs(a - b).max() for a, b in zip(C_g, C_o)) / scale
+    assert err_c <= tol_c, f"covariance blocks rel err {err_c:.2e}"
+    assert np.allclose(mean.cpu().numpy(), m_o, rtol=1e-6, atol=1e-6 * np.abs(m_o).max())
+    lam_g, U_g = F.split_eig(plan, evals.cpu().numpy(), evecs.cpu().numpy())
+    pool_o = sorted(((-l, k, i) for k, lk in enumerate(lam_o) for i, l in enumerate(lk)))[:50]
+    worst = max(abs(lam_g[k][i] - lam_o[k][i]) / abs(lam_o[k][i]) for _, k, i in pool_o)
+    assert worst <= 1e-4, f"top-50 eigenvalue rel err {worst:.2e}"
+    for k in sorted({k for _, k, _ in pool_o}):
+        r = sum(1 for _, kk, _ in pool_o if kk == k)
+        assert _subspace_cos(U_g[k], U_o[k], lam_o[k], r) >= 0.9999, f"subspace k={k}"
+    return err_c, worst
+
+
+def test_c3_full_size_spectral_parity():
+    """configs[2] at full size (100,000 images): GPU K5/K6 against the fp64 oracle K5/K6 run on the GPU's own
+    coefficients (K1-K4 are checked by sampled coefficient parity, K5-K7 this way)."""
+    cfg = synth.config("C3")
+    n = cfg["n"]
+    imgs = synth.blob_images(cfg, 0, n, device=DEV)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0)
+    coeffs = F.fbspca_expand(plan, imgs)
+    del imgs
+    blocks, mean = F.fbspca_covariance(plan, coeffs)
+    evals, evecs = F.fbspca_eig(plan, blocks)
+    torch.cuda.synchronize()
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    m_o, C_o = _oracle_cov_from_gpu_coeffs(coeffs, basis)
+    _spectral_checks(plan, blocks, mean, evals, evecs, m_o, C_o)
+
+
+@pytest.mark.parametrize("name,n", [("C4", 2048), ("C5", 1024)])
+def test_large_L_spectral_parity_subset(name, n):
+    """configs[3] (L = 256, pow2 kernels, R = 128 tensor-core covariance) and configs[4] (L = 360, runtime
+    mixed-radix FFTs, p_k up to 179): a subset of images through K1-K6, oracle K5/K6 on the GPU coefficients."""
+    cfg, imgs = blob_case(name, 0, n)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=512)
+    coeffs = F.fbspca_expand(plan, imgs)
+    blocks, mean = F.fbspca_covariance(plan, coeffs)
+    evals, evecs = F.fbspca_eig(plan, blocks)
+    torch.cuda.synchronize()
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    m_o, C_o = _oracle_cov_from_gpu_coeffs(coeffs, basis)
+    _spectral_checks(plan, blocks, mean, evals, evecs, m_o, C_o)
