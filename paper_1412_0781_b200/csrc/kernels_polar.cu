@@ -109,7 +109,9 @@ template <typename T2> struct Dft<T2, 5> {
 // DFT_R, writes st((j / Ns) Ns R + (j mod Ns) + r Ns).  Out of place; one warp; R values in registers.
 // Twiddles come from a per-stage table tws[TOFF + (r - 1) Ns + (j mod Ns)] (contiguous in j: no bank
 // conflicts), built once per CTA by build_stage_tw<N>.
-template <typename T2, int N, int R, int Ns, int TOFF, class Ld, class St>
+// HZ (first stage only): inputs t in [N/4, 3N/4) are known zeros -- the zero-padded rows / columns of K1
+// (pixel index L/2 <= M/4 away from 0 on both sides) -- so those butterfly legs are constant zeros.
+template <typename T2, int N, int R, int Ns, int TOFF, class Ld, class St, bool HZ = false>
 __device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tws, int lane) {
   constexpr int NB = N / R;
 #pragma unroll
@@ -118,7 +120,10 @@ __device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tws,
     if (NB % 32 == 0 || j < NB) {
       T2 v[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[r] = ld(j + r * NB);
+      for (int r = 0; r < R; ++r) {
+        if (HZ && R >= 4 && r >= R / 4 && r < 3 * R / 4) v[r] = T2{0, 0};
+        else v[r] = ld(j + r * NB);
+      }
       const int jm = j & (Ns - 1);
       if constexpr (Ns > 1) {
 #pragma unroll
@@ -172,25 +177,25 @@ __device__ void build_stage_tw(T2* dst, const T2* __restrict__ lin, int tid, int
 }
 
 // Compile-time power-of-two FFT: first stage reads ld(), last stage writes st(), ping-pong in A, B.
-template <typename T2, int N, class Ld, class St>
+template <typename T2, int N, bool HZ = false, class Ld, class St>
 __device__ __forceinline__ void fft_pow2(Ld ld, St st, T2* A, T2* B, const T2* tw, int lane) {
   auto lA = [A](int i) { return A[padi(i)]; };
   auto lB = [B](int i) { return B[padi(i)]; };
   auto sA = [A](int i, T2 v) { A[padi(i)] = v; };
   auto sB = [B](int i, T2 v) { B[padi(i)] = v; };
   if constexpr (N == 64) {
-    cstage<T2, 64, 8, 1, 0>(ld, sA, tw, lane); cstage<T2, 64, 8, 8, 0>(lA, st, tw, lane);
+    cstage<T2, 64, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 64, 8, 8, 0>(lA, st, tw, lane);
   } else if constexpr (N == 128) {
-    cstage<T2, 128, 8, 1, 0>(ld, sA, tw, lane); cstage<T2, 128, 4, 8, 0>(lA, sB, tw, lane);
+    cstage<T2, 128, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 128, 4, 8, 0>(lA, sB, tw, lane);
     cstage<T2, 128, 4, 32, 24>(lB, st, tw, lane);
   } else if constexpr (N == 256) {
-    cstage<T2, 256, 8, 1, 0>(ld, sA, tw, lane); cstage<T2, 256, 8, 8, 0>(lA, sB, tw, lane);
+    cstage<T2, 256, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 256, 8, 8, 0>(lA, sB, tw, lane);
     cstage<T2, 256, 4, 64, 56>(lB, st, tw, lane);
   } else if constexpr (N == 512) {
-    cstage<T2, 512, 8, 1, 0>(ld, sA, tw, lane); cstage<T2, 512, 8, 8, 0>(lA, sB, tw, lane);
+    cstage<T2, 512, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 512, 8, 8, 0>(lA, sB, tw, lane);
     cstage<T2, 512, 8, 64, 56>(lB, st, tw, lane);
   } else if constexpr (N == 1024) {
-    cstage<T2, 1024, 8, 1, 0>(ld, sA, tw, lane); cstage<T2, 1024, 8, 8, 0>(lA, sB, tw, lane);
+    cstage<T2, 1024, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 1024, 8, 8, 0>(lA, sB, tw, lane);
     cstage<T2, 1024, 4, 64, 56>(lB, sA, tw, lane); cstage<T2, 1024, 4, 256, 248>(lA, st, tw, lane);
   } else {
     static_assert(N == 64, "unsupported compile-time FFT size");
@@ -246,9 +251,9 @@ __device__ void fft_rt(const FftPlan& f, Ld ld, St st, T2* A, T2* B, const T2* t
   }
 }
 
-template <typename T2, int NC, class Ld, class St>
+template <typename T2, int NC, bool HZ = false, class Ld, class St>
 __device__ __forceinline__ void fft_any(const FftPlan& f, Ld ld, St st, T2* A, T2* B, const T2* tw, int lane) {
-  if constexpr (NC > 0) fft_pow2<T2, NC>(ld, st, A, B, tw, lane);
+  if constexpr (NC > 0) fft_pow2<T2, NC, HZ>(ld, st, A, B, tw, lane);
   else fft_rt<T2>(f, ld, st, A, B, tw, lane);
 }
 
@@ -404,7 +409,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         // runtime sizes: the result goes to a per-warp slice of the (still free) phase region.
         T2* res = (MC > 0) ? (fft_result_in_A<MC>() ? myA : myB) : region + (size_t)warp * M;
         auto st = [res](int i, T2 v) { res[MC > 0 ? padi(i) : i] = v; };
-        fft_any<T2, MC>(pp.fft_M, ld, st, myA, myB, twM, lane);
+        fft_any<T2, MC, true>(pp.fft_M, ld, st, myA, myB, twM, lane);
         const int lo0 = pp.phase_lo[0], hi0 = lo0 + (S < col_lo + ncx - lo0 ? S : col_lo + ncx - lo0);
         const int lo1 = pp.n_phase > 1 ? pp.phase_lo[1] : (1 << 30);
         for (int cc = lane; cc < ncx; cc += 32) {
@@ -464,7 +469,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             if (m1 < -M / 2 + PADR) col[(size_t)(m1 + M + row0) * S] = v;
             if (m1 >= M / 2 - PADR) col[(size_t)(m1 - M + row0) * S] = v;
           };
-          fft_any<T2, MC>(pp.fft_M, ld, st, myA, myB, twM, lane);
+          fft_any<T2, MC, true>(pp.fft_M, ld, st, myA, myB, twM, lane);
         }
       }
       __syncthreads();
