@@ -7,6 +7,7 @@
  *   Algorithm 1  fbspca_expand      images -> FB coefficients a_{k,q}
  *   Algorithm 2  fbspca_covariance  C^(k) = Re(A_k A_k^*)/n, mean at k=0 only
  *                            fbspca_eig         C^(k) = U_k diag(lambda^(k)) U_k^T
+ *                            fbspca_radial_eigenfunctions  f^{k,l}(xi_j) (Alg. 2 line 5)
  *                            fbspca_project     c^i_{k,l} = sum_q a^i_{k,q} u_l^(k)(q) (+ filter)
  *
  * Conventions (all fixed):
@@ -122,6 +123,13 @@ fbspca_status fbspca_allreduce_partial(fbspca_plan_t plan, double* d_partial, vo
  * Synchronises the stream to check convergence (<= 30 sweeps); FBSPCA_ERR_NUMERIC names the block. */
 fbspca_status fbspca_eig(fbspca_plan_t plan, const double* d_blocks, double* d_evals, double* d_evecs,
                          fbspca_stream_t stream);
+
+/* Alg. 2 line 5, Eq. (sPCArad): the radial eigenfunctions at the plan's GL nodes xi_j,
+ *   f^{k,l}(xi_j) = sum_q u_l^(k)(q) N_{k,q} J_k(R_{k,q} xi_j / c),   fp64.
+ * d_evecs: eigenvectors as written by fbspca_eig (evec_off layout).  d_f: coef_off[k_max+1] x n_xi doubles,
+ * row coef_off[k] + l (l = 0..p_k-1), column j (xi_j from fbspca_plan_detail).  Asynchronous. */
+fbspca_status fbspca_radial_eigenfunctions(fbspca_plan_t plan, const double* d_evecs, double* d_f,
+                                           fbspca_stream_t stream);
 
 /* Alg. 2 line 6 (Eq. (sPCAcoeff)) with optional filtering:
  *   out_k[l][i] = h^(k)_l sum_q u_l^(k)(q) (a^i_{k,q} - [k=0] m_q)

@@ -22,7 +22,7 @@ __all__ = [
     "radial_table", "polar_ft_direct", "angular_transform", "radial_quadrature",
     "expand", "expand_polar", "synthesize_polar", "mean_and_center",
     "block_covariance", "covariance_partials", "finalize_covariance",
-    "block_eig", "sign_normalize", "spca_coeffs", "mp_edge", "mp_select",
+    "block_eig", "sign_normalize", "radial_eigenfunctions", "spca_coeffs", "mp_edge", "mp_select",
     "shrink_weights", "project", "rotate_coeffs", "reflect_coeffs",
     "flat_index", "to_flat", "from_flat",
 ]
@@ -286,6 +286,20 @@ def block_eig(C: list):
         lam.append(w[o])
         U.append(sign_normalize(V[:, o]))
     return lam, U
+
+
+def radial_eigenfunctions(basis: Basis, U: list, xi=None) -> list:
+    """Alg. 2 line 5, Eq. (sPCArad) P:360-361:
+    f^{k,l}(xi_j) = sum_q N_{k,q} J_k(R_{k,q} xi_j / c) u_l^(k)(q), at the GL nodes xi_j (default);
+    returns (p_k, n_xi) per k, row l."""
+    if xi is None:
+        xi, _, _ = polar_grid(basis)
+    out = []
+    for k in range(basis.k_max + 1):
+        Rk = basis.zeros[k][: basis.p[k]]
+        Bk = basis.norm[k][:, None] * jv(k, np.outer(Rk, xi) / basis.c)      # [q][j]
+        out.append(U[k].T @ Bk)
+    return out
 
 
 # --------------------------------------------------------------------------

@@ -30,6 +30,7 @@ SIGNATURES = {
     "fbspca_covariance_accumulate": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "fbspca_allreduce_partial": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "fbspca_eig": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "fbspca_radial_eigenfunctions": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "fbspca_project": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_double, c_int, c_int64,
                                c_void_p, c_void_p]),
     "fbspca_nccl_unique_id": (c_int, [c_void_p]),

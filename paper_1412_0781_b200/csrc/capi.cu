@@ -152,6 +152,7 @@ fbspca_status upload_plan(Plan& P) {
     auto tt = twiddles<double2, double>(P.n_theta);
     FB_CUDA(upload(&P.d_tw_theta, tt.data(), tt.size()), "upload twiddles");
   }
+  FB_CUDA(upload((void**)&P.d_rbasis, P.rbasis.data(), P.rbasis.size()), "upload radial basis");
   FB_CUDA(upload((void**)&P.d_rho, P.rho.data(), P.rho.size()), "upload rho");
   FB_CUDA(upload((void**)&P.d_cs, P.cs.data(), P.cs.size()), "upload cs");
   FB_CUDA(upload((void**)&P.d_nodes, P.nodes.data(), P.nodes.size()), "upload nodes");
@@ -193,7 +194,7 @@ void free_plan(Plan& P) {
   DeviceGuard g(P.device);
   void* ptrs[] = {P.d_table, P.d_deapod, P.d_tw_M, P.d_tw_theta, P.d_rho, P.d_cs, P.d_nodes, P.d_xscratch,
                   P.d_pscratch, P.d_ghat, P.d_partial, P.d_p, P.d_coef_off, P.d_blk_off, P.d_evec_off,
-                  P.d_eig_work, P.d_eig_sweeps, P.d_coef_k, P.d_pp, P.d_cov_scratch, P.d_cov_scratch0, P.d_table_hi, P.d_table_lo,
+                  P.d_eig_work, P.d_eig_sweeps, P.d_coef_k, P.d_pp, P.d_cov_scratch, P.d_cov_scratch0, P.d_table_hi, P.d_table_lo, P.d_rbasis,
                   P.d_noderec, P.d_dnoderec};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& ev : P.tevents) { cudaEventDestroy(ev.second.first); cudaEventDestroy(ev.second.second); }
@@ -386,6 +387,18 @@ fbspca_status fbspca_eig(fbspca_plan_t h, const double* d_blocks, double* d_eval
       set_error("Jacobi did not converge within 30 sweeps for block k = " + std::to_string(k));
       return FBSPCA_ERR_NUMERIC;
     }
+  return FBSPCA_OK;
+}
+
+fbspca_status fbspca_radial_eigenfunctions(fbspca_plan_t h, const double* d_evecs, double* d_f,
+                                           fbspca_stream_t stream) {
+  fbspca_status st = check_compute_plan(h);
+  if (st != FBSPCA_OK) return st;
+  Plan& P = *h;
+  if (!d_evecs || !d_f) { set_error("radial_eigenfunctions: null pointer"); return FBSPCA_ERR_ARG; }
+  if (!aligned(d_evecs, 8) || !aligned(d_f, 8)) { set_error("radial_eigenfunctions: misaligned pointer"); return FBSPCA_ERR_ARG; }
+  DeviceGuard g(P.device);
+  FB_CUDA(launch_radial_eigfun(P, d_evecs, d_f, (cudaStream_t)stream), "radial eigenfunction kernel");
   return FBSPCA_OK;
 }
 

@@ -79,6 +79,7 @@ struct Plan {
   int n_xi = 0, n_theta = 0;
   std::vector<double> xi, wq;
   std::vector<double> table;             // [coef row][j]: N J_k(R xi_j/c) xi_j w_j (2 pi / n_theta)
+  std::vector<double> rbasis;            // [coef row][j]: N J_k(R xi_j/c)  (Eq. (sPCArad))
   // NUFFT
   int M = 0, w = 0;
   double beta = 0;
@@ -92,6 +93,7 @@ struct Plan {
   int polar_grid = 0;                    // resident CTAs of the polar kernel
   // device buffers
   void* d_table = nullptr;               // T (float or double), coef rows x n_xi
+  double* d_rbasis = nullptr;            // rbasis (fp64), coef rows x n_xi
   float* d_table_lo = nullptr;           // fp32 plans: T - tf32(T)  (3xTF32 tensor-core K4)
   float* d_table_hi = nullptr;           // fp32 plans: tf32_rna(T)
   bool use_tc = true;                    // K4 on tcgen05 (fp32 plans)
@@ -143,6 +145,7 @@ cudaError_t launch_cov_finalize(const Plan& P, const double* d_partial, double* 
                                 cudaStream_t s);
 cudaError_t launch_eig(const Plan& P, const double* d_blocks, double* d_evals, double* d_evecs,
                        cudaStream_t s);
+cudaError_t launch_radial_eigfun(const Plan& P, const double* d_evecs, double* d_f, cudaStream_t s);
 cudaError_t launch_project(const Plan& P, const void* d_coeffs, int64_t n, const double* d_mean,
                            const double* d_evals, const double* d_evecs, double sigma2, int mode,
                            int64_t n_total, void* d_out, cudaStream_t s);

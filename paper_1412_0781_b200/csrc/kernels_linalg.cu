@@ -374,6 +374,31 @@ cudaError_t launch_eig(const Plan& P, const double* d_blocks, double* d_evals, d
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- Alg. 2 line 5: Eq. (sPCArad)
+// f^{k,l}(xi_j) = sum_q u_l^(k)(q) N_{k,q} J_k(R_{k,q} xi_j / c)  (fp64), one CTA per k (U_k and the basis read
+// through L1/L2: p_k^2 <= 179^2 doubles does not always fit shared memory; the step is O(sum p_k^2 n_xi), tiny).
+// Output row (coef_off[k] + l), column j (n_xi per row).
+__global__ void __launch_bounds__(256)
+radial_eigfun_kernel(const double* __restrict__ evecs, const double* __restrict__ rbasis, const int* __restrict__ p,
+                     const int64_t* __restrict__ coef_off, const int64_t* __restrict__ evec_off, int n_xi,
+                     double* __restrict__ f) {
+  const int k = blockIdx.x, pk = p[k];
+  const double* Uk = evecs + evec_off[k];
+  const double* Bk = rbasis + coef_off[k] * n_xi;
+  double* Fk = f + coef_off[k] * n_xi;
+  for (int e = threadIdx.x; e < pk * n_xi; e += blockDim.x) {
+    const int l = e / n_xi, j = e - l * n_xi;
+    double s = 0.0;
+    for (int q = 0; q < pk; ++q) s = fma(__ldg(Uk + q * pk + l), __ldg(Bk + (int64_t)q * n_xi + j), s);
+    Fk[e] = s;
+  }
+}
+
+cudaError_t launch_radial_eigfun(const Plan& P, const double* d_evecs, double* d_f, cudaStream_t s) {
+  radial_eigfun_kernel<<<P.k_max + 1, 256, 0, s>>>(d_evecs, P.d_rbasis, P.d_p, P.d_coef_off, P.d_evec_off, P.n_xi, d_f);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- K7: Eq. (sPCAcoeff) P:364 + filter P:689-699
 template <typename T>
 __global__ void __launch_bounds__(256)

@@ -236,13 +236,18 @@ fbspca_status build_host_plan(Plan& P) {
   gauss_legendre(P.n_xi, 0.0, c, P.xi, P.wq);
   const int64_t ncoef = P.coef_off[nk];
   P.table.assign(size_t(ncoef) * P.n_xi, 0.0);
+  P.rbasis.assign(size_t(ncoef) * P.n_xi, 0.0);
   const double ang = 2 * M_PI / P.n_theta;        // Eq. (1DFFT) weight, folded into the table
   for (int k = 0; k < nk; ++k)
     for (int q = 0; q < P.p[k]; ++q) {
       int64_t row = P.coef_off[k] + q;
       double Rq = P.zeros[row], N = P.norm[row];
       for (int j = 0; j < P.n_xi; ++j)
-        P.table[row * P.n_xi + j] = N * bessel_j(k, Rq * P.xi[j] / c) * P.xi[j] * P.wq[j] * ang;
+      {
+        const double b = N * bessel_j(k, Rq * P.xi[j] / c);            // N_{k,q} J_k(R_{k,q} xi_j / c)
+        P.rbasis[row * P.n_xi + j] = b;
+        P.table[row * P.n_xi + j] = b * P.xi[j] * P.wq[j] * ang;
+      }
     }
 
   // ---- NUFFT: oversampled grid, window, deapodisation ----

@@ -175,6 +175,14 @@ def fbspca_eig(plan: Plan, blocks: torch.Tensor, stream=None):
     return evals, evecs
 
 
+def fbspca_radial_eigenfunctions(plan: Plan, evecs: torch.Tensor, stream=None) -> torch.Tensor:
+    """Alg. 2 line 5: f^{k,l}(xi_j) as a (sum_k p_k) x n_xi fp64 tensor (row coef_off[k] + l)."""
+    f = torch.empty((plan.n_coef, plan.n_xi), dtype=torch.float64, device=evecs.device)
+    check(lib().fbspca_radial_eigenfunctions(ctypes.c_void_p(plan.handle), _ptr(evecs), _ptr(f), _stream_ptr(stream)),
+          "fbspca_radial_eigenfunctions")
+    return f
+
+
 def fbspca_project(plan: Plan, coeffs: torch.Tensor, mean, evals, evecs, sigma2: float = 0.0, mode: int = 0,
                    n_total: int | None = None, out=None, stream=None) -> torch.Tensor:
     n = coeffs.shape[1]

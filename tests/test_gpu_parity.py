@@ -315,3 +315,27 @@ def test_large_L_spectral_parity_subset(name, n):
     basis = O.build_basis(cfg["c"], cfg["R"])
     m_o, C_o = _oracle_cov_from_gpu_coeffs(coeffs, basis)
     _spectral_checks(plan, blocks, mean, evals, evecs, m_o, C_o)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C5"])
+def test_radial_eigenfunctions_parity(name):
+    """Alg. 2 line 5 (Eq. (sPCArad)): GPU f^{k,l}(xi_j) from the GPU eigenvectors vs the oracle's
+    f^{k,l} from the same eigenvectors (fp64 both: 1e-10), on random SPD blocks."""
+    cfg = synth.config(name)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=16)
+    rng = np.random.default_rng(21)
+    packed = np.zeros(plan.n_blk)
+    for k in range(plan.k_max + 1):
+        pk = int(plan.p[k])
+        X = rng.standard_normal((pk, pk + 2))
+        packed[plan.blk_off[k]:plan.blk_off[k + 1]] = (X @ X.T)[np.triu_indices(pk)]
+    evals, evecs = F.fbspca_eig(plan, torch.from_numpy(packed).to(DEV))
+    f = F.fbspca_radial_eigenfunctions(plan, evecs)
+    torch.cuda.synchronize()
+    _, U_g = F.split_eig(plan, evals.cpu().numpy(), evecs.cpu().numpy())
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    f_o = O.radial_eigenfunctions(basis, U_g)
+    got = f.cpu().numpy()
+    for k in range(basis.k_max + 1):
+        fk = got[plan.coef_off[k]:plan.coef_off[k + 1]]
+        assert np.max(np.abs(fk - f_o[k])) <= 1e-10 * max(1.0, np.abs(f_o[k]).max()), f"k={k}"

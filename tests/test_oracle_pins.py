@@ -382,3 +382,44 @@ def test_covariance_shard_partials_and_invariance():
     for T in (O.rotate_coeffs(A, 1.1), O.reflect_coeffs(A, 0.4)):
         _, C3 = O.block_covariance(T)
         assert all(np.allclose(x, y, atol=1e-12) for x, y in zip(C, C3))
+
+
+# ---------------------------------------------------------------- Alg. 2 line 5: radial eigenfunctions
+def test_radial_eigenfunctions_basis_and_permutation():
+    """U = permutation: f^{k,l} is exactly the Bessel basis function N J_k(R_{k,pi(l)} xi / c) (Eq. (sPCArad)),
+    evaluated here from scipy's jn_zeros / jv -- catches a transposed U (pi vs pi^-1) or a dropped norm."""
+    b = O.build_basis(0.5, 16)
+    xi, _, _ = O.polar_grid(b)
+    rng = np.random.default_rng(3)
+    U, perms = [], []
+    for k in range(b.k_max + 1):
+        pi = rng.permutation(b.p[k])
+        P = np.zeros((b.p[k], b.p[k]))
+        P[pi, np.arange(b.p[k])] = 1.0                 # u_l(q) = [q == pi(l)]
+        U.append(P)
+        perms.append(pi)
+    f = O.radial_eigenfunctions(b, U)
+    for k in (0, 1, 7, b.k_max):
+        z = jn_zeros(k, b.p[k])
+        for l in range(b.p[k]):
+            q = perms[k][l]
+            ref = jv(k, z[q] * xi / b.c) / (b.c * math.sqrt(math.pi) * abs(jv(k + 1, z[q])))
+            assert np.allclose(f[k][l], ref, rtol=1e-10, atol=1e-12)
+
+
+def test_radial_eigenfunctions_orthonormal_and_consistent():
+    """For orthogonal U_k the f^{k,l} are orthonormal, 2 pi int_0^c f f' xi dxi = delta (Bessel orthonormality,
+    P:87; 600-point GL rule, exact here), and sum_l c_{k,l} f^{k,l} = sum_q a_{k,q} N J_k(R_q xi/c) (Eq. (sPCAcoeff))."""
+    b = O.build_basis(0.5, 12)
+    rng = np.random.default_rng(5)
+    U = [np.linalg.qr(rng.standard_normal((pk, pk)))[0] for pk in b.p]
+    x, w = O.gauss_legendre(600, 0.0, b.c)
+    f = O.radial_eigenfunctions(b, U, xi=x)
+    for k in range(b.k_max + 1):
+        G = 2 * np.pi * (f[k] * (x * w)[None, :]) @ f[k].T
+        assert np.max(np.abs(G - np.eye(b.p[k]))) < 1e-11
+    a = [rng.standard_normal((pk, 3)) + 1j * rng.standard_normal((pk, 3)) for pk in b.p]
+    c = O.spca_coeffs(a, U)
+    f0 = O.radial_eigenfunctions(b, [np.eye(pk) for pk in b.p], xi=x)   # the Bessel basis itself
+    for k in (0, 2, b.k_max):
+        assert np.allclose(f[k].T @ c[k], f0[k].T @ a[k], atol=1e-11)
