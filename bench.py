@@ -101,7 +101,8 @@ def work_per_image(plan, L):
     """Algorithmic flops of K1-K3 (polar kernel) and bytes of each stage, per image."""
     M, w, nxi, nth, kmax = plan.M, plan.w, plan.n_xi, plan.n_theta, plan.k_max
     lg = lambda n: math.log2(n)
-    k1 = 5 * M * lg(M) * (L / 2) + 5 * M * lg(M) * (M / 4 + w)       # row FFTs (L/2 complex) + column FFTs
+    ncx = M // 2 + w                                                  # grid columns the half-plane gather reads
+    k1 = 5 * M * lg(M) * (L / 2) + 5 * M * lg(M) * ncx              # row FFTs (L/2 complex) + those columns' FFTs
     k2 = nxi * (nth // 2) * w * w * 4                                 # complex-by-real taps
     k3 = nxi * 5 * nth * lg(nth)                                      # ring FFTs
     ncoef = plan.n_coef
