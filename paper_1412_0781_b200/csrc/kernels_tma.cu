@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -543,7 +544,11 @@ cudaError_t launch_radial_tma(const Plan& P, int64_t nb, int64_t i0, int64_t ld,
   a.bmax = bbox;                                           // B tiles sized for the largest box
   const int stage = 128 * ROWB + 2 * bbox * ROWB;
   const int fixed = 2 * 128 * ROWB + 1024 + 256;
-  a.stages = std::max(2, std::min(8, (227 * 1024 - fixed) / stage));
+  // two CTAs per SM when each still gets >= 3 stages (two independent TMA / MMA pipelines per SM)
+  const char* env = getenv("FBSPCA_K4_CTAS");
+  const int per_sm = env ? std::max(1, std::min(2, atoi(env))) : ((113 * 1024 - fixed) / stage >= 3 ? 2 : 1);
+  const int budget = (per_sm == 2 ? 113 : 227) * 1024;
+  a.stages = std::max(2, std::min(8, (budget - fixed) / stage));
   const int smem = a.stages * stage + fixed;
   static int configured = 0;
   if (configured < smem) {
@@ -552,7 +557,7 @@ cudaError_t launch_radial_tma(const Plan& P, int64_t nb, int64_t i0, int64_t ld,
     configured = smem;
   }
   const int items = nk * a.nrt;
-  const int grid = std::min(items, P.num_sms);
+  const int grid = std::min(items, per_sm * P.num_sms);
   radial_tma_kernel<<<grid, 320, smem, s>>>(ta, tbh, tbl, a);
   return cudaGetLastError();
 }
