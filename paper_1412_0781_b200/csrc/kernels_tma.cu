@@ -327,7 +327,7 @@ struct K5Args {
 };
 
 template <int RR>   // register accumulators per thread (= largest box b of k >= 1)
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(192, RR <= 64 ? 2 : 1)
 cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   // 1024-B aligned base by pointer arithmetic on the shared array (keeps the shared address space for the compiler)
@@ -438,23 +438,19 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
       bar_wait(&accfull[a], (gg >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t tb = tmem + (uint32_t(32 * warp) << 16) + uint32_t(a * 2 * RR);
-      // 32 columns of X and Y in flight per wait (b is a power of two >= 16)
+      // 16 columns of X and Y in flight per wait (b is a power of two >= 16; few registers: 2 CTAs per SM)
 #pragma unroll
-      for (int c1 = 0; c1 < RR; c1 += 32) {
+      for (int c1 = 0; c1 < RR; c1 += 16) {
         if (c1 < b) {
-          uint32_t xr[32], yr[32];
-          const bool two = c1 + 16 < b;
+          uint32_t xr[16], yr[16];
           tmem_ld16_nowait(tb + uint32_t(c1), xr);
           tmem_ld16_nowait(tb + uint32_t(b + c1), yr);
-          if (two) { tmem_ld16_nowait(tb + uint32_t(c1 + 16), xr + 16); tmem_ld16_nowait(tb + uint32_t(b + c1 + 16), yr + 16); }
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
+          for (int i = 0; i < 16; ++i) {
             const int c = c1 + i;
-            if (i < 16 || two) {
-              const float xv = __uint_as_float(xr[i]), yv = __uint_as_float(yr[i]);
-              acc[c] += c > q ? yv : c == q ? xv + 2.f * yv : xv + yv;
-            }
+            const float xv = __uint_as_float(xr[i]), yv = __uint_as_float(yr[i]);
+            acc[c] += c > q ? yv : c == q ? xv + 2.f * yv : xv + yv;
           }
         }
       }
@@ -566,10 +562,13 @@ cudaError_t launch_radial_tma(const Plan& P, int64_t nb, int64_t i0, int64_t ld,
 template <int RR>
 static cudaError_t launch_cov_tma_t(const Plan& P, const MapSet& ta, K5Args& a, cudaStream_t s) {
   const int fixed = RR * (RR + 1) * 4 + 1024 + 256;
+  const char* env = getenv("FBSPCA_K5_CTAS");
+  const int per_sm = env ? std::max(1, std::min(2, atoi(env))) : 2;
+  const int budget = (per_sm == 2 ? 113 : 227) * 1024;
   a.ck = K5_CK;                                            // fewer chunks per stage when a tile is 32 KB
-  while (a.ck > 1 && 3 * a.ck * std::max(128, 2 * RR) * ROWB > 227 * 1024 - fixed) a.ck /= 2;
+  while (a.ck > 1 && 2 * a.ck * std::max(128, 2 * RR) * ROWB > budget - fixed) a.ck /= 2;
   const int stage = a.ck * std::max(128, 2 * RR) * ROWB;
-  a.stages = std::max(2, std::min(8, (227 * 1024 - fixed) / stage));
+  a.stages = std::max(2, std::min(8, (budget - fixed) / stage));
   const int smem = a.stages * stage + fixed;
   static int configured = 0;
   if (configured < smem) {
@@ -578,7 +577,7 @@ static cudaError_t launch_cov_tma_t(const Plan& P, const MapSet& ta, K5Args& a, 
     configured = smem;
   }
   const int items = a.k_max * a.nchunk;
-  const int grid = std::min(items, P.num_sms);
+  const int grid = std::min(items, per_sm * P.num_sms);
   cov_tma_kernel<RR><<<grid, 192, smem, s>>>(ta, a);
   return cudaGetLastError();
 }
