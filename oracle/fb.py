@@ -23,7 +23,7 @@ __all__ = [
     "expand", "expand_polar", "synthesize_polar", "mean_and_center",
     "block_covariance", "covariance_partials", "finalize_covariance",
     "block_eig", "sign_normalize", "radial_eigenfunctions", "spca_coeffs", "mp_edge", "mp_select",
-    "shrink_weights", "project", "rotate_coeffs", "reflect_coeffs",
+    "shrink_weights", "project", "backproject", "synthesize_pixels", "rotate_coeffs", "reflect_coeffs",
     "flat_index", "to_flat", "from_flat",
 ]
 
@@ -353,6 +353,46 @@ def project(A: list, mean: np.ndarray, U: list, lam: list, basis: Basis,
     c = spca_coeffs(Ac, U)
     h = shrink_weights(lam, basis, n_total, sigma2, mode)
     return [hk[:, None] * ck for hk, ck in zip(h, c)]
+
+
+def backproject(c: list, mean: np.ndarray, U: list) -> list:
+    """Steerable-basis coefficients back to FB coefficients: a_k = U_k c_k (U_k orthogonal, so this inverts
+    Eq. (sPCAcoeff)), plus the mean at k = 0 (Alg. 2 line 1 undone).  With c = filtered coefficients
+    (project(mode 1/2)) this gives the FB coefficients of the denoised images."""
+    out = [Uk @ ck for Uk, ck in zip(U, c)]
+    out[0] = out[0] + mean[:, None]
+    return out
+
+
+def synthesize_pixels(A: list, basis: Basis, L: int, mask: bool = True) -> np.ndarray:
+    """Images from FB coefficients on the L x L pixel grid (NEXT-1: eigenimages, denoised images):
+    I(x) = sum_q a_{0,q} F^-1 psi^{0,q}(x) + 2 Re sum_{k>=1,q} a_{k,q} F^-1 psi^{k,q}(x)   (a_{-k} = conj a_k)
+    with Eq. (IFT_FB) read with i^{+k} in the numerator (Q2):
+      F^-1 psi^{k,q}(r, phi) = 2 c sqrt(pi) (-1)^q R_{k,q} i^k J_k(2 pi c r) e^{ik phi} / ((2 pi c r)^2 - R_{k,q}^2),
+    (q = 1..p_k), removable singularity c sqrt(pi) (-1)^{q+1} i^k J_{k+1}(R_{k,q}) e^{ik phi}; pixels with r > R
+    are zero when mask (the compact support of P:115).  Axis 0 = i1 = x (Q3).  Returns (n, L, L) float64."""
+    idx = np.arange(L) - L // 2
+    i1, i2 = np.meshgrid(idx, idx, indexing="ij")
+    r = np.hypot(i1, i2).ravel()
+    phi = np.arctan2(i2, i1).ravel()
+    keep = (r <= basis.R) if mask else np.ones(r.shape, dtype=bool)
+    x = 2 * np.pi * basis.c * r
+    n = A[0].shape[1]
+    img = np.zeros((n, L * L))
+    for k in range(basis.k_max + 1):
+        ang = (1j ** k) * np.exp(1j * k * phi)
+        for q in range(basis.p[k]):
+            Rq = basis.zeros[k][q]
+            den = x * x - Rq * Rq
+            near = np.abs(x - Rq) < 1e-8
+            val = 2 * basis.c * np.sqrt(np.pi) * (-1) ** (q + 1) * Rq * jv(k, x) / np.where(near, 1.0, den)
+            val = np.where(near, basis.c * np.sqrt(np.pi) * (-1) ** (q + 2) * jv(k + 1, Rq), val)
+            psi = val * ang * keep
+            if k == 0:
+                img += np.outer(A[0][q].real, psi.real)
+            else:
+                img += 2.0 * np.real(np.outer(A[k][q], psi))
+    return img.reshape(n, L, L)
 
 
 # --------------------------------------------------------------------------

@@ -423,3 +423,38 @@ def test_radial_eigenfunctions_orthonormal_and_consistent():
     f0 = O.radial_eigenfunctions(b, [np.eye(pk) for pk in b.p], xi=x)   # the Bessel basis itself
     for k in (0, 2, b.k_max):
         assert np.allclose(f[k].T @ c[k], f0[k].T @ a[k], atol=1e-11)
+
+
+# ---------------------------------------------------------------- NEXT-1: pixel synthesis and back-projection
+def test_synthesize_pixels_recovery_and_rotation():
+    """O.synthesize_pixels (Eq. (IFT_FB), reading Q2) is inverted by the oracle's expansion up to the truncation
+    error of the finite grid, which shrinks with zero padding (prefactor, sign, orientation, q-parity pinned:
+    the (-1)^q with the paper's q = 1..p_k); rot90 of the image = a_k e^{-ik pi/2} at odd L."""
+    b = O.build_basis(0.5, 16)
+    rng = np.random.default_rng(12)
+    v = [np.exp(-b.zeros[k][: b.p[k]] ** 2 / 200.0) for k in range(b.k_max + 1)]
+    a = [np.sqrt(v[0])[:, None] * rng.standard_normal((b.p[0], 3)) + 0j] + \
+        [np.sqrt(vk / 2)[:, None] * (rng.standard_normal((len(vk), 3)) + 1j * rng.standard_normal((len(vk), 3)))
+         for vk in v[1:]]
+    errs = []
+    for L in (32, 64):
+        img = O.synthesize_pixels(a, b, L, mask=False)
+        got = O.expand(img, b)
+        errs.append(np.linalg.norm(O.to_flat(got) - O.to_flat(a)) / np.linalg.norm(O.to_flat(a)))
+    assert errs[0] < 1e-2 and errs[1] < 0.3 * errs[0]
+    img = O.synthesize_pixels(a, b, 33)
+    rot = O.synthesize_pixels(O.rotate_coeffs(a, np.pi / 2), b, 33)
+    assert np.allclose(rot, np.rot90(img, k=1, axes=(1, 2)), atol=1e-12 * np.abs(img).max())
+
+
+def test_backproject_inverts_projection():
+    """backproject(spca_coeffs(centred a, U), mean, U) = a for orthogonal U (Eq. (sPCAcoeff) P:364 inverted)."""
+    b = O.build_basis(0.5, 12)
+    rng = np.random.default_rng(13)
+    a = [rng.standard_normal((pk, 4)) + 1j * rng.standard_normal((pk, 4)) for pk in b.p]
+    a[0] = a[0].real + 0j
+    mean, Ac = O.mean_and_center(a)
+    U = [np.linalg.qr(rng.standard_normal((pk, pk)))[0] for pk in b.p]
+    back = O.backproject(O.spca_coeffs(Ac, U), mean, U)
+    for x, y in zip(back, a):
+        assert np.allclose(x, y, atol=1e-12)
