@@ -8,6 +8,8 @@
  *   Algorithm 2  fbspca_covariance  C^(k) = Re(A_k A_k^*)/n, mean at k=0 only
  *                            fbspca_eig         C^(k) = U_k diag(lambda^(k)) U_k^T
  *                            fbspca_radial_eigenfunctions  f^{k,l}(xi_j) (Alg. 2 line 5)
+ *   NEXT-1 (denoising)       fbspca_backproject  a_k = U_k c_k (+ mean): filtered steerable coefficients -> FB
+ *                            fbspca_synthesize   FB coefficients -> pixel images (Eq. (IFT_FB))
  *                            fbspca_project     c^i_{k,l} = sum_q a^i_{k,q} u_l^(k)(q) (+ filter)
  *
  * Conventions (all fixed):
@@ -140,6 +142,22 @@ fbspca_status fbspca_radial_eigenfunctions(fbspca_plan_t plan, const double* d_e
 fbspca_status fbspca_project(fbspca_plan_t plan, const void* d_coeffs, int64_t n, const double* d_mean,
                              const double* d_evals, const double* d_evecs, double sigma2, int mode,
                              int64_t n_total, void* d_out, fbspca_stream_t stream);
+
+/* NEXT-1: a_k = U_k c_k, plus m at k = 0 (Im kept 0) -- inverts Eq. (sPCAcoeff) P:364 for orthogonal U_k and undoes
+ * the centring of Alg. 2 line 1.  With d_c = fbspca_project(mode 1 or 2) output these are the FB coefficients of
+ * the denoised images.  d_c, d_coeffs_out: coefficient layout, ld = n (may not alias); d_mean p_0
+ * doubles, d_evecs as from fbspca_eig.  Asynchronous. */
+fbspca_status fbspca_backproject(fbspca_plan_t plan, const void* d_c, int64_t n, const double* d_mean,
+                                 const double* d_evecs, void* d_coeffs_out, fbspca_stream_t stream);
+
+/* NEXT-1: images from FB coefficients on the L x L pixel grid, Eq. (IFT_FB) P:108 read with i^{+k} in the
+ * numerator (reading Q2): I(x) = sum_q a_{0,q} rho_{0,q}(r) + 2 Re sum_{k>=1,q} a_{k,q} rho_{k,q}(r) i^k e^{ik phi},
+ * rho_{k,q}(r) = 2 c sqrt(pi) (-1)^q R_{k,q} J_k(2 pi c r) / ((2 pi c r)^2 - R_{k,q}^2) (q = 1..p_k), for pixels with
+ * r <= R (zero elsewhere, the compact support P:115); axis 0 = i1 (Q3).  fp64 arithmetic.  d_coeffs: coefficient
+ * layout, ld = n.  d_images: n x L x L (float or double per dt), n <= 65535 per call.  The first call builds
+ * the plan's radial tables (host, synchronous).  Asynchronous otherwise. */
+fbspca_status fbspca_synthesize(fbspca_plan_t plan, const void* d_coeffs, int64_t n, void* d_images,
+                                fbspca_stream_t stream);
 
 /* NCCL plumbing (libnccl.so.2 is dlopen'ed on first use).  unique_id: 128 bytes. */
 fbspca_status fbspca_nccl_unique_id(void* unique_id_out);

@@ -381,11 +381,12 @@ def synthesize_pixels(A: list, basis: Basis, L: int, mask: bool = True) -> np.nd
     img = np.zeros((n, L * L))
     for k in range(basis.k_max + 1):
         ang = (1j ** k) * np.exp(1j * k * phi)
+        jk = jv(k, x)                                   # J_k(2 pi c r): the same for every q
         for q in range(basis.p[k]):
             Rq = basis.zeros[k][q]
             den = x * x - Rq * Rq
             near = np.abs(x - Rq) < 1e-8
-            val = 2 * basis.c * np.sqrt(np.pi) * (-1) ** (q + 1) * Rq * jv(k, x) / np.where(near, 1.0, den)
+            val = 2 * basis.c * np.sqrt(np.pi) * (-1) ** (q + 1) * Rq * jk / np.where(near, 1.0, den)
             val = np.where(near, basis.c * np.sqrt(np.pi) * (-1) ** (q + 2) * jv(k + 1, Rq), val)
             psi = val * ang * keep
             if k == 0:

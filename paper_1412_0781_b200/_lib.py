@@ -31,6 +31,8 @@ SIGNATURES = {
     "fbspca_allreduce_partial": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "fbspca_eig": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "fbspca_radial_eigenfunctions": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "fbspca_backproject": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "fbspca_synthesize": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "fbspca_project": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_double, c_int, c_int64,
                                c_void_p, c_void_p]),
     "fbspca_nccl_unique_id": (c_int, [c_void_p]),

@@ -7,7 +7,7 @@ import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-SRC = ["csrc/plan.cpp", "csrc/kernels_polar.cu", "csrc/kernels_linalg.cu", "csrc/kernels_tma.cu", "csrc/capi.cu"]
+SRC = ["csrc/plan.cpp", "csrc/kernels_polar.cu", "csrc/kernels_linalg.cu", "csrc/kernels_tma.cu", "csrc/kernels_synth.cu", "csrc/capi.cu"]
 HDR = ["csrc/internal.h", os.path.join("..", "include", "fbspca.h")]
 LIB = os.path.join(PKG, "lib", "libfbspca.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -195,6 +195,7 @@ void free_plan(Plan& P) {
   void* ptrs[] = {P.d_table, P.d_deapod, P.d_tw_M, P.d_tw_theta, P.d_rho, P.d_cs, P.d_nodes, P.d_xscratch,
                   P.d_pscratch, P.d_ghat, P.d_partial, P.d_p, P.d_coef_off, P.d_blk_off, P.d_evec_off,
                   P.d_eig_work, P.d_eig_sweeps, P.d_coef_k, P.d_pp, P.d_cov_scratch, P.d_cov_scratch0, P.d_table_hi, P.d_table_lo, P.d_rbasis,
+                  P.d_synth_rho, P.d_synth_pidx, P.d_synth_pir, P.d_synth_pcs, P.d_synth_grp,
                   P.d_noderec, P.d_dnoderec};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& ev : P.tevents) { cudaEventDestroy(ev.second.first); cudaEventDestroy(ev.second.second); }
@@ -399,6 +400,32 @@ fbspca_status fbspca_radial_eigenfunctions(fbspca_plan_t h, const double* d_evec
   if (!aligned(d_evecs, 8) || !aligned(d_f, 8)) { set_error("radial_eigenfunctions: misaligned pointer"); return FBSPCA_ERR_ARG; }
   DeviceGuard g(P.device);
   FB_CUDA(launch_radial_eigfun(P, d_evecs, d_f, (cudaStream_t)stream), "radial eigenfunction kernel");
+  return FBSPCA_OK;
+}
+
+fbspca_status fbspca_synthesize(fbspca_plan_t h, const void* d_coeffs, int64_t n, void* d_images,
+                                fbspca_stream_t stream) {
+  fbspca_status st = check_compute_plan(h);
+  if (st != FBSPCA_OK) return st;
+  Plan& P = *h;
+  const size_t rsz = P.dt == FBSPCA_F32 ? 4 : 8;
+  if (!d_coeffs || !d_images || n < 1) { set_error("synthesize: null pointer or n < 1"); return FBSPCA_ERR_ARG; }
+  if (!aligned(d_coeffs, 2 * rsz) || !aligned(d_images, rsz)) { set_error("synthesize: misaligned pointer"); return FBSPCA_ERR_ARG; }
+  if (n > 65535) { set_error("synthesize: n > 65535 per call"); return FBSPCA_ERR_ARG; }
+  DeviceGuard g(P.device);
+  FB_CUDA(launch_synthesize(P, d_coeffs, n, d_images, (cudaStream_t)stream), "synthesis kernel");
+  return FBSPCA_OK;
+}
+
+fbspca_status fbspca_backproject(fbspca_plan_t h, const void* d_c, int64_t n, const double* d_mean,
+                                 const double* d_evecs, void* d_coeffs_out, fbspca_stream_t stream) {
+  fbspca_status st = check_compute_plan(h);
+  if (st != FBSPCA_OK) return st;
+  Plan& P = *h;
+  if (!d_c || !d_mean || !d_evecs || !d_coeffs_out || n < 1) { set_error("backproject: bad argument"); return FBSPCA_ERR_ARG; }
+  if (d_c == d_coeffs_out) { set_error("backproject: output aliases input"); return FBSPCA_ERR_ARG; }
+  DeviceGuard g(P.device);
+  FB_CUDA(launch_backproject(P, d_c, n, d_mean, d_evecs, d_coeffs_out, (cudaStream_t)stream), "backproject kernel");
   return FBSPCA_OK;
 }
 

@@ -126,6 +126,13 @@ struct Plan {
   std::vector<float> tms;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> tevents;
   int num_sms = 0;
+  // NEXT-1 synthesis tables (built on the first fbspca_synthesize)
+  double* d_synth_rho = nullptr;         // [coef row][radius]: rho_{k,q}(r)
+  int* d_synth_pidx = nullptr;           // disk pixels sorted by radius: linear index, radius index, (cos, sin) phi
+  int* d_synth_pir = nullptr;
+  double* d_synth_pcs = nullptr;
+  int* d_synth_grp = nullptr;            // pixel groups of <= 2048 (CTA work units)
+  int synth_nr = 0, synth_ngroups = 0;
   cudaStream_t side = nullptr;           // K5: the k = 0 fp64 CTAs run here, forked from / joined to the caller's stream
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
@@ -146,6 +153,9 @@ cudaError_t launch_cov_finalize(const Plan& P, const double* d_partial, double* 
 cudaError_t launch_eig(const Plan& P, const double* d_blocks, double* d_evals, double* d_evecs,
                        cudaStream_t s);
 cudaError_t launch_radial_eigfun(const Plan& P, const double* d_evecs, double* d_f, cudaStream_t s);
+cudaError_t launch_synthesize(Plan& P, const void* d_coeffs, int64_t n, void* d_images, cudaStream_t s);
+cudaError_t launch_backproject(const Plan& P, const void* d_c, int64_t n, const double* d_mean, const double* d_evecs,
+                               void* d_out, cudaStream_t s);
 cudaError_t launch_project(const Plan& P, const void* d_coeffs, int64_t n, const double* d_mean,
                            const double* d_evals, const double* d_evecs, double sigma2, int mode,
                            int64_t n_total, void* d_out, cudaStream_t s);

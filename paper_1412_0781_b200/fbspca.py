@@ -183,6 +183,27 @@ def fbspca_radial_eigenfunctions(plan: Plan, evecs: torch.Tensor, stream=None) -
     return f
 
 
+def fbspca_backproject(plan: Plan, c: torch.Tensor, mean, evecs, out=None, stream=None) -> torch.Tensor:
+    """NEXT-1: a_k = U_k c_k (+ mean at k = 0), coefficient layout in and out."""
+    n = c.shape[1]
+    if out is None:
+        out = torch.empty_like(c)
+    check(lib().fbspca_backproject(ctypes.c_void_p(plan.handle), _ptr(c), n, _ptr(mean), _ptr(evecs), _ptr(out),
+                                   _stream_ptr(stream)), "fbspca_backproject")
+    return out
+
+
+def fbspca_synthesize(plan: Plan, coeffs: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    """NEXT-1: n x L x L images from FB coefficients (Eq. (IFT_FB), reading Q2), zero outside r <= R."""
+    n = coeffs.shape[1]
+    if out is None:
+        dt = torch.float32 if plan.dtype == F32 else torch.float64
+        out = torch.empty((n, plan.L, plan.L), dtype=dt, device=coeffs.device)
+    check(lib().fbspca_synthesize(ctypes.c_void_p(plan.handle), _ptr(coeffs), n, _ptr(out), _stream_ptr(stream)),
+          "fbspca_synthesize")
+    return out
+
+
 def fbspca_project(plan: Plan, coeffs: torch.Tensor, mean, evals, evecs, sigma2: float = 0.0, mode: int = 0,
                    n_total: int | None = None, out=None, stream=None) -> torch.Tensor:
     n = coeffs.shape[1]

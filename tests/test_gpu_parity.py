@@ -339,3 +339,56 @@ def test_radial_eigenfunctions_parity(name):
     for k in range(basis.k_max + 1):
         fk = got[plan.coef_off[k]:plan.coef_off[k + 1]]
         assert np.max(np.abs(fk - f_o[k])) <= 1e-10 * max(1.0, np.abs(f_o[k]).max()), f"k={k}"
+
+
+# ------------------------------------------------------------------ NEXT-1: back to pixels (denoising)
+@pytest.mark.parametrize("name,n", [("C1", 6), ("C2", 5), ("C3", 3)])
+def test_synthesize_parity(name, n):
+    """fbspca_synthesize (Eq. (IFT_FB), reading Q2) vs O.synthesize_pixels on the same random coefficients."""
+    cfg = synth.config(name)
+    dt = F.F64 if cfg["dtype"] == "f64" else F.F32
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], dtype=dt, device=0, max_batch=16)
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    rng = np.random.default_rng(31)
+    a = [rng.standard_normal((pk, n)) + 1j * rng.standard_normal((pk, n)) for pk in basis.p]
+    a[0] = a[0].real + 0j
+    flat = O.to_flat(a)
+    ct = torch.from_numpy(flat.astype(np.complex128 if dt == F.F64 else np.complex64)).to(DEV)
+    img = F.fbspca_synthesize(plan, ct)
+    torch.cuda.synchronize()
+    ref = O.synthesize_pixels(O.from_flat(flat.astype(np.complex64).astype(np.complex128) if dt == F.F32 else flat,
+                                          basis), basis, cfg["L"])
+    got = img.cpu().numpy().astype(np.float64)
+    tol = 1e-10 if dt == F.F64 else 1e-5
+    assert np.max(np.abs(got - ref)) <= tol * np.abs(ref).max()
+
+
+def test_denoise_pipeline_parity_c2():
+    """NEXT-1 end to end on C2 images: expand -> covariance -> eig -> project(mode 1: MP + Wiener) ->
+    backproject -> synthesize, each GPU stage fed the previous GPU stage, vs the oracle stage on the same inputs."""
+    cfg, imgs = blob_case("C2", 0, 600)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=256)
+    coeffs = F.fbspca_expand(plan, imgs)
+    blocks, mean = F.fbspca_covariance(plan, coeffs)
+    evals, evecs = F.fbspca_eig(plan, blocks)
+    sigma2 = float(synth.blobs.noise_sigma(cfg, device=DEV)) ** 2
+    chat = F.fbspca_project(plan, coeffs, mean, evals, evecs, sigma2=sigma2, mode=1)
+    ahat = F.fbspca_backproject(plan, chat, mean, evecs)
+    den = F.fbspca_synthesize(plan, ahat[:, :8].contiguous())
+    torch.cuda.synchronize()
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    lam_g, U_g = F.split_eig(plan, evals.cpu().numpy(), evecs.cpu().numpy())
+    c_g = O.from_flat(chat.cpu().numpy().astype(np.complex128), basis)
+    a_ref = O.backproject(c_g, mean.cpu().numpy(), U_g)
+    a_got = O.from_flat(ahat.cpu().numpy().astype(np.complex128), basis)
+    for x, y in zip(a_got, a_ref):
+        assert np.allclose(x, y, atol=1e-5 * max(1.0, np.abs(y).max()))
+    ref = O.synthesize_pixels([x[:, :8] for x in O.from_flat(ahat.cpu().numpy().astype(np.complex128), basis)],
+                              basis, cfg["L"])
+    assert np.max(np.abs(den.cpu().numpy() - ref)) <= 1e-5 * np.abs(ref).max()
+    # denoising reduces the error to the clean images inside the support (the paper's use case, P:699)
+    clean = synth.blob_images(cfg, 0, 8, device=DEV, sigma_n=0.0).cpu().numpy()
+    idx = np.arange(cfg["L"]) - cfg["L"] // 2
+    disk = (idx[:, None] ** 2 + idx[None, :] ** 2) <= cfg["R"] ** 2
+    noisy = imgs[:8].cpu().numpy()
+    assert np.linalg.norm((den.cpu().numpy() - clean)[:, disk]) < 0.5 * np.linalg.norm((noisy - clean)[:, disk])
