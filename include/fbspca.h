@@ -10,6 +10,7 @@
  *                            fbspca_radial_eigenfunctions  f^{k,l}(xi_j) (Alg. 2 line 5)
  *   NEXT-1 (denoising)       fbspca_backproject  a_k = U_k c_k (+ mean): filtered steerable coefficients -> FB
  *                            fbspca_synthesize   FB coefficients -> pixel images (Eq. (IFT_FB))
+ *   NEXT-2 (parameters)      fbspca_estimate_params  sigma^2, R, c from a stack
  *                            fbspca_project     c^i_{k,l} = sum_q a^i_{k,q} u_l^(k)(q) (+ filter)
  *
  * Conventions (all fixed):
@@ -158,6 +159,20 @@ fbspca_status fbspca_backproject(fbspca_plan_t plan, const void* d_c, int64_t n,
  * the plan's radial tables (host, synchronous).  Asynchronous otherwise. */
 fbspca_status fbspca_synthesize(fbspca_plan_t plan, const void* d_coeffs, int64_t n, void* d_images,
                                 fbspca_stream_t stream);
+
+/* NEXT-2 (Fig. 5): noise variance, support radius and band limit of an image stack, as the paper
+ * picks R = 98 and c = 0.196 for its ribosome images.  Per-pixel mean and variance (one streaming pass) and the
+ * mean power spectrum of the mean-subtracted images, |DFT2|^2 / L^2 (white noise of variance s^2 sits at s^2), are
+ * formed on the GPU (fp64 accumulation); radial averages in bins b = floor(r + 1/2) (pixel offsets a - floor(L/2),
+ * integer frequencies) are formed on the host, then
+ *   sigma2 = mean variance over radius bins ceil(0.45 L) <= b < floor(L/2)   (the outer 10 % of radii below L/2),
+ *   R      = smallest b with sum_{b' <= b} max(var_b' - sigma2, 0) b'  >= fraction x its total over b < floor(L/2),
+ *   c      = b / L for the smallest frequency bin 1 <= b <= floor(L/2) with the same rule on the power spectrum.
+ * d_images: n x L x L (float or double per dt) on `device`; L must be 2^a 3^b 5^c; n >= 2; 0 < fraction <= 1
+ * (the paper uses 0.999).  Synchronous; allocates and frees its own scratch (this is not a plan call).
+ * FBSPCA_ERR_NUMERIC when no variance / power exceeds the noise level (pure noise). */
+fbspca_status fbspca_estimate_params(int L, fbspca_dtype dt, int device, const void* d_images, int64_t n,
+                                     double fraction, double* sigma2, double* R, double* c);
 
 /* NCCL plumbing (libnccl.so.2 is dlopen'ed on first use).  unique_id: 128 bytes. */
 fbspca_status fbspca_nccl_unique_id(void* unique_id_out);

@@ -25,6 +25,7 @@ __all__ = [
     "block_eig", "sign_normalize", "radial_eigenfunctions", "spca_coeffs", "mp_edge", "mp_select",
     "shrink_weights", "project", "backproject", "synthesize_pixels", "rotate_coeffs", "reflect_coeffs",
     "flat_index", "to_flat", "from_flat",
+    "radial_profile", "estimate_noise_variance", "estimate_support", "estimate_bandlimit",
 ]
 
 
@@ -425,3 +426,62 @@ def to_flat(A: list) -> np.ndarray:
 def from_flat(flat: np.ndarray, basis: Basis) -> list:
     off = basis.coef_off
     return [flat[off[k]:off[k + 1]] for k in range(basis.k_max + 1)]
+
+
+# --------------------------------------------------------------------------
+# NEXT-2: parameter estimation (Fig. 5; SPEC estimate_noise_variance / _support / _bandlimit)
+# --------------------------------------------------------------------------
+def radial_profile(m: np.ndarray, offsets: np.ndarray, nbins: int, weights=None) -> np.ndarray:
+    """Mean of a 2-D map over bins b = floor(r + 1/2), r = |(o1, o2)| of the given per-axis offsets (reading Q18)."""
+    o1, o2 = np.meshgrid(offsets, offsets, indexing="ij")
+    b = np.floor(np.hypot(o1, o2) + 0.5).astype(int)
+    w = np.ones_like(m) if weights is None else weights
+    out = np.zeros(nbins)
+    for k in range(nbins):
+        sel = b == k
+        out[k] = (m[sel] * w[sel]).sum() / w[sel].sum() if sel.any() else 0.0
+    return out
+
+
+def _variance_profile(stack: np.ndarray) -> np.ndarray:
+    L = stack.shape[1]
+    var = ((stack - stack.mean(axis=0)) ** 2).mean(axis=0)           # divisor n (Q9's convention)
+    return radial_profile(var, np.arange(L) - L // 2, L // 2)
+
+
+def estimate_noise_variance(stack: np.ndarray) -> float:
+    """sigma^2 = mean of the angularly averaged variance of the mean-subtracted images over the outer 10 % of
+    radii below L/2: bins ceil(0.45 L) <= b < floor(L/2)  ("levels off at ... the noise variance"; Q19)."""
+    L = stack.shape[1]
+    prof = _variance_profile(stack)
+    return float(prof[int(np.ceil(0.45 * L - 1e-12)):].mean())
+
+
+def _fraction_point(w: np.ndarray, frac: float) -> int:
+    tot = w.sum()
+    if not tot > 0:
+        raise ValueError("no signal above the noise level")
+    return int(np.argmax(np.cumsum(w) >= frac * tot))
+
+
+def estimate_support(stack: np.ndarray, sigma2: float, fraction: float = 0.999) -> float:
+    """R = smallest radius bin at which the cumulative sum of max(var_b - sigma^2, 0) b (Jacobian r dr) reaches the
+    fraction of its total over b < floor(L/2)  ("99.9% at r = 98")."""
+    prof = _variance_profile(stack)
+    b = np.arange(len(prof))
+    return float(_fraction_point(np.maximum(prof - sigma2, 0.0) * b, fraction))
+
+
+def estimate_bandlimit(stack: np.ndarray, sigma2: float, fraction: float = 0.999) -> float:
+    """c = b / L for the smallest frequency bin 1 <= b <= floor(L/2) at which the cumulative sum of
+    max(P_b - sigma^2, 0) b (Jacobian xi dxi) reaches the fraction of its total; P = mean |DFT2(I - mean)|^2 / L^2
+    (white noise of variance s^2 -> level s^2, Q20), binned over integer frequencies ("c = 0.196")."""
+    n, L, _ = stack.shape
+    X = np.fft.fft2(stack - stack.mean(axis=0), axes=(1, 2))
+    P = (np.abs(X) ** 2).mean(axis=0) / (L * L)
+    f = np.round(np.fft.fftfreq(L) * L)
+    prof = radial_profile(P, f, L // 2 + 1)
+    b = np.arange(len(prof))
+    w = np.maximum(prof - sigma2, 0.0) * b
+    w[0] = 0.0
+    return float(_fraction_point(w, fraction)) / L

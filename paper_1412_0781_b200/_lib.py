@@ -33,6 +33,7 @@ SIGNATURES = {
     "fbspca_radial_eigenfunctions": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "fbspca_backproject": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "fbspca_synthesize": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
+    "fbspca_estimate_params": (c_int, [c_int, c_int, c_int, c_void_p, c_int64, c_double, P_double, P_double, P_double]),
     "fbspca_project": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_double, c_int, c_int64,
                                c_void_p, c_void_p]),
     "fbspca_nccl_unique_id": (c_int, [c_void_p]),

@@ -445,6 +445,19 @@ fbspca_status fbspca_project(fbspca_plan_t h, const void* d_coeffs, int64_t n, c
   return FBSPCA_OK;
 }
 
+fbspca_status fbspca_estimate_params(int L, fbspca_dtype dt, int device, const void* d_images, int64_t n,
+                                     double fraction, double* sigma2, double* R, double* c) {
+  if (!d_images || !sigma2 || !R || !c) { set_error("estimate_params: null pointer"); return FBSPCA_ERR_ARG; }
+  if (L < 16 || n < 2 || !(fraction > 0 && fraction <= 1) || (dt != FBSPCA_F32 && dt != FBSPCA_F64)) {
+    set_error("estimate_params: need L >= 16, n >= 2, 0 < fraction <= 1"); return FBSPCA_ERR_ARG;
+  }
+  DeviceGuard g(device);
+  double out[3];
+  fbspca_status st = estimate_params(L, dt, device, d_images, n, fraction, out);
+  *sigma2 = out[0]; *R = out[1]; *c = out[2];
+  return st;
+}
+
 fbspca_status fbspca_nccl_unique_id(void* out) {
   if (!out) { set_error("null out"); return FBSPCA_ERR_ARG; }
   if (!nccl_load()) return FBSPCA_ERR_NCCL;

@@ -156,6 +156,8 @@ cudaError_t launch_radial_eigfun(const Plan& P, const double* d_evecs, double* d
 cudaError_t launch_synthesize(Plan& P, const void* d_coeffs, int64_t n, void* d_images, cudaStream_t s);
 cudaError_t launch_backproject(const Plan& P, const void* d_c, int64_t n, const double* d_mean, const double* d_evecs,
                                void* d_out, cudaStream_t s);
+fbspca_status estimate_params(int L, fbspca_dtype dt, int device, const void* d_images, int64_t n, double fraction,
+                              double* out3);
 cudaError_t launch_project(const Plan& P, const void* d_coeffs, int64_t n, const double* d_mean,
                            const double* d_evals, const double* d_evecs, double sigma2, int mode,
                            int64_t n_total, void* d_out, cudaStream_t s);

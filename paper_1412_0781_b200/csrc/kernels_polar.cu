@@ -14,248 +14,10 @@
 // Polar samples go to a per-CTA L2-resident scratch and are read back by the angular pass.
 #include <cuda_runtime.h>
 
+#include "fft_device.cuh"
 #include "internal.h"
 
 namespace fbspca {
-
-template <typename T> struct Cx;
-template <> struct Cx<float> { using t = float2; };
-template <> struct Cx<double> { using t = double2; };
-
-template <typename T2> __device__ __forceinline__ T2 cadd(T2 a, T2 b) { return {a.x + b.x, a.y + b.y}; }
-template <typename T2> __device__ __forceinline__ T2 csub(T2 a, T2 b) { return {a.x - b.x, a.y - b.y}; }
-template <typename T2> __device__ __forceinline__ T2 cmul(T2 a, T2 b) {
-  return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
-}
-template <typename T2> __device__ __forceinline__ T2 mul_mi(T2 a) { return {a.y, -a.x}; }   // -i * a
-
-// acc + w g for a real weight w: one packed FFMA2 (fma.rn.f32x2, w broadcast) in fp32, two FMAs in fp64
-__device__ __forceinline__ float2 rfma(float w, float2 g, float2 acc) {
-  unsigned long long r, gg, aa, ww;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(gg) : "f"(g.x), "f"(g.y));
-  asm("mov.b64 %0, {%1, %2};" : "=l"(aa) : "f"(acc.x), "f"(acc.y));
-  asm("mov.b64 %0, {%1, %1};" : "=l"(ww) : "f"(w));
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(ww), "l"(gg), "l"(aa));
-  float2 o;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
-  return o;
-}
-__device__ __forceinline__ double2 rfma(double w, double2 g, double2 acc) {
-  return {fma(w, g.x, acc.x), fma(w, g.y, acc.y)};
-}
-
-// ---------------------------------------------------------------- small forward DFTs (e^{-2 pi i})
-template <typename T2, int R> struct Dft;
-template <typename T2> struct Dft<T2, 2> {
-  __device__ __forceinline__ static void run(T2* v) { T2 a = v[0]; v[0] = cadd(a, v[1]); v[1] = csub(a, v[1]); }
-};
-template <typename T2> struct Dft<T2, 4> {
-  __device__ __forceinline__ static void run(T2* v) {
-    T2 s0 = cadd(v[0], v[2]), d0 = csub(v[0], v[2]);
-    T2 s1 = cadd(v[1], v[3]), d1 = mul_mi(csub(v[1], v[3]));
-    v[0] = cadd(s0, s1); v[2] = csub(s0, s1);
-    v[1] = cadd(d0, d1); v[3] = csub(d0, d1);
-  }
-};
-template <typename T2> struct Dft<T2, 8> {
-  __device__ __forceinline__ static void run(T2* v) {
-    using T = decltype(v[0].x);
-    const T h = T(0.70710678118654752440);
-    T2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
-    Dft<T2, 4>::run(e); Dft<T2, 4>::run(o);
-    // twiddles e^{-2 pi i k / 8}, k = 0..3
-    T2 t1 = {h * (o[1].x + o[1].y), h * (o[1].y - o[1].x)};
-    T2 t2 = mul_mi(o[2]);
-    T2 t3 = {h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y)};
-    v[0] = cadd(e[0], o[0]); v[4] = csub(e[0], o[0]);
-    v[1] = cadd(e[1], t1);   v[5] = csub(e[1], t1);
-    v[2] = cadd(e[2], t2);   v[6] = csub(e[2], t2);
-    v[3] = cadd(e[3], t3);   v[7] = csub(e[3], t3);
-  }
-};
-template <typename T2> struct Dft<T2, 3> {
-  __device__ __forceinline__ static void run(T2* v) {
-    using T = decltype(v[0].x);
-    const T c1 = T(-0.5), s1 = T(-0.86602540378443864676);   // e^{-2 pi i/3}
-    T2 s = cadd(v[1], v[2]), d = csub(v[1], v[2]);
-    T2 a = {v[0].x + c1 * s.x, v[0].y + c1 * s.y};
-    T2 b = {-s1 * d.y, s1 * d.x};                                // i s1 d
-    v[0] = cadd(v[0], s);
-    v[1] = cadd(a, b);
-    v[2] = csub(a, b);
-  }
-};
-template <typename T2> struct Dft<T2, 5> {
-  __device__ __forceinline__ static void run(T2* v) {
-    using T = decltype(v[0].x);
-    const T c1 = T(0.30901699437494742410), c2 = T(-0.80901699437494742410);
-    const T s1 = T(-0.95105651629515357212), s2 = T(-0.58778525229247312917);   // sin(-2pi k/5)
-    T2 a1 = cadd(v[1], v[4]), b1 = csub(v[1], v[4]);
-    T2 a2 = cadd(v[2], v[3]), b2 = csub(v[2], v[3]);
-    T2 x0 = v[0];
-    v[0] = cadd(x0, cadd(a1, a2));
-    T2 r1 = {x0.x + c1 * a1.x + c2 * a2.x, x0.y + c1 * a1.y + c2 * a2.y};
-    T2 r2 = {x0.x + c2 * a1.x + c1 * a2.x, x0.y + c2 * a1.y + c1 * a2.y};
-    // i * (s1 b1 + s2 b2) and i * (s2 b1 - s1 b2)
-    T2 i1 = {-(s1 * b1.y + s2 * b2.y), s1 * b1.x + s2 * b2.x};
-    T2 i2 = {-(s2 * b1.y - s1 * b2.y), s2 * b1.x - s1 * b2.x};
-    v[1] = cadd(r1, i1); v[4] = csub(r1, i1);
-    v[2] = cadd(r2, i2); v[3] = csub(r2, i2);
-  }
-};
-
-// ---------------------------------------------------------------- warp FFTs with load/store functors
-// Stockham (autosort) stage of radix R: butterfly j reads ld(j + r NB), twiddles by w^(r (j mod Ns)),
-// DFT_R, writes st((j / Ns) Ns R + (j mod Ns) + r Ns).  Out of place; one warp; R values in registers.
-// Twiddles come from a per-stage table tws[TOFF + (r - 1) Ns + (j mod Ns)] (contiguous in j: no bank
-// conflicts), built once per CTA by build_stage_tw<N>.
-// HZ (first stage only): inputs t in [N/4, 3N/4) are known zeros -- the zero-padded rows / columns of K1
-// (pixel index L/2 <= M/4 away from 0 on both sides) -- so those butterfly legs are constant zeros.
-template <typename T2, int N, int R, int Ns, int TOFF, class Ld, class St, bool HZ = false>
-__device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tws, int lane) {
-  constexpr int NB = N / R;
-#pragma unroll
-  for (int j0 = 0; j0 < NB; j0 += 32) {
-    const int j = j0 + lane;
-    if (NB % 32 == 0 || j < NB) {
-      T2 v[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if (HZ && R >= 4 && r >= R / 4 && r < 3 * R / 4) v[r] = T2{0, 0};
-        else v[r] = ld(j + r * NB);
-      }
-      const int jm = j & (Ns - 1);
-      if constexpr (Ns > 1) {
-#pragma unroll
-        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tws[TOFF + (r - 1) * Ns + jm]);
-      }
-      Dft<T2, R>::run(v);
-      const int idxD = (j - jm) * R + jm;
-#pragma unroll
-      for (int r = 0; r < R; ++r) st(idxD + r * Ns, v[r]);
-    }
-  }
-  __syncwarp();
-}
-
-// Ping-pong scratch index swizzle: XOR the low 4 bits with 3 (i >> 4).  64-bit shared accesses resolve per
-// half-warp; this mapping keeps every load/store pattern of the stages below at 1.03x the ideal wavefronts
-// (unswizzled: 2.1x).
-__device__ __forceinline__ int padi(int i) { return i ^ ((3 * (i >> 4)) & 15); }
-
-// which ping-pong buffer the last stage of fft_pow2<N> does NOT read (so the result may be stored there)
-template <int N> __host__ __device__ constexpr bool fft_result_in_A() { return N == 128 || N == 256 || N == 512; }
-
-// stage list per size: (R, Ns) ... ; table offsets TOFF accumulate (R - 1) Ns over stages with Ns > 1
-template <typename T2, int R, int Ns>
-__device__ __forceinline__ void fill_stage_tw(T2* dst, const T2* __restrict__ lin, int N, int tid, int nthr) {
-  const int step = N / (Ns * R);
-  for (int e = tid; e < (R - 1) * Ns; e += nthr) {
-    const int r = 1 + e / Ns, jm = e % Ns;
-    dst[e] = lin[jm * step * r];
-  }
-}
-template <int N> constexpr int stage_tw_len() {
-  return N == 64 ? 56 : N == 128 ? 120 : N == 256 ? 248 : N == 512 ? 504 : N == 1024 ? 1016 : N;
-}
-template <typename T2, int N>
-__device__ void build_stage_tw(T2* dst, const T2* __restrict__ lin, int tid, int nthr) {
-  if constexpr (N == 64) {
-    fill_stage_tw<T2, 8, 8>(dst, lin, N, tid, nthr);
-  } else if constexpr (N == 128) {
-    fill_stage_tw<T2, 4, 8>(dst, lin, N, tid, nthr); fill_stage_tw<T2, 4, 32>(dst + 24, lin, N, tid, nthr);
-  } else if constexpr (N == 256) {
-    fill_stage_tw<T2, 8, 8>(dst, lin, N, tid, nthr); fill_stage_tw<T2, 4, 64>(dst + 56, lin, N, tid, nthr);
-  } else if constexpr (N == 512) {
-    fill_stage_tw<T2, 8, 8>(dst, lin, N, tid, nthr); fill_stage_tw<T2, 8, 64>(dst + 56, lin, N, tid, nthr);
-  } else if constexpr (N == 1024) {
-    fill_stage_tw<T2, 8, 8>(dst, lin, N, tid, nthr); fill_stage_tw<T2, 4, 64>(dst + 56, lin, N, tid, nthr);
-    fill_stage_tw<T2, 4, 256>(dst + 248, lin, N, tid, nthr);
-  } else {
-    for (int i = tid; i < N; i += nthr) dst[i] = lin[i];     // runtime path: linear table
-  }
-}
-
-// Compile-time power-of-two FFT: first stage reads ld(), last stage writes st(), ping-pong in A, B.
-template <typename T2, int N, bool HZ = false, class Ld, class St>
-__device__ __forceinline__ void fft_pow2(Ld ld, St st, T2* A, T2* B, const T2* tw, int lane) {
-  auto lA = [A](int i) { return A[padi(i)]; };
-  auto lB = [B](int i) { return B[padi(i)]; };
-  auto sA = [A](int i, T2 v) { A[padi(i)] = v; };
-  auto sB = [B](int i, T2 v) { B[padi(i)] = v; };
-  if constexpr (N == 64) {
-    cstage<T2, 64, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 64, 8, 8, 0>(lA, st, tw, lane);
-  } else if constexpr (N == 128) {
-    cstage<T2, 128, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 128, 4, 8, 0>(lA, sB, tw, lane);
-    cstage<T2, 128, 4, 32, 24>(lB, st, tw, lane);
-  } else if constexpr (N == 256) {
-    cstage<T2, 256, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 256, 8, 8, 0>(lA, sB, tw, lane);
-    cstage<T2, 256, 4, 64, 56>(lB, st, tw, lane);
-  } else if constexpr (N == 512) {
-    cstage<T2, 512, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 512, 8, 8, 0>(lA, sB, tw, lane);
-    cstage<T2, 512, 8, 64, 56>(lB, st, tw, lane);
-  } else if constexpr (N == 1024) {
-    cstage<T2, 1024, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 1024, 8, 8, 0>(lA, sB, tw, lane);
-    cstage<T2, 1024, 4, 64, 56>(lB, sA, tw, lane); cstage<T2, 1024, 4, 256, 248>(lA, st, tw, lane);
-  } else {
-    static_assert(N == 64, "unsupported compile-time FFT size");
-  }
-}
-
-// Runtime mixed-radix (2,3,4,5,8) version for sizes without a compile-time path (e.g. 720, 1440).
-template <typename T2, int R, class Ld, class St>
-__device__ __forceinline__ void rstage(Ld ld, St st, int N, int Ns, const T2* __restrict__ tw, int lane) {
-  const int NB = N / R, step = N / (Ns * R);
-  for (int j = lane; j < NB; j += 32) {
-    T2 v[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = ld(j + r * NB);
-    const int jm = j % Ns;
-#pragma unroll
-    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[jm * step * r]);
-    Dft<T2, R>::run(v);
-    const int idxD = (j - jm) * R + jm;
-#pragma unroll
-    for (int r = 0; r < R; ++r) st(idxD + r * Ns, v[r]);
-  }
-  __syncwarp();
-}
-
-template <typename T2, class Ld, class St>
-__device__ __forceinline__ void rstage_any(int R, Ld ld, St st, int N, int Ns, const T2* tw, int lane) {
-  switch (R) {
-    case 8: rstage<T2, 8>(ld, st, N, Ns, tw, lane); break;
-    case 4: rstage<T2, 4>(ld, st, N, Ns, tw, lane); break;
-    case 2: rstage<T2, 2>(ld, st, N, Ns, tw, lane); break;
-    case 5: rstage<T2, 5>(ld, st, N, Ns, tw, lane); break;
-    default: rstage<T2, 3>(ld, st, N, Ns, tw, lane); break;
-  }
-}
-
-template <typename T2, class Ld, class St>
-__device__ void fft_rt(const FftPlan& f, Ld ld, St st, T2* A, T2* B, const T2* tw, int lane) {
-  auto lA = [A](int i) { return A[padi(i)]; };
-  auto lB = [B](int i) { return B[padi(i)]; };
-  auto sA = [A](int i, T2 v) { A[padi(i)] = v; };
-  auto sB = [B](int i, T2 v) { B[padi(i)] = v; };
-  const int last = f.nstages - 1;
-  int Ns = 1;
-  for (int s = 0; s <= last; ++s) {
-    const int R = f.radix[s];
-    const bool in_A = (s & 1);          // stage s >= 1 reads the buffer written by stage s-1
-    if (s == 0 && s == last) rstage_any<T2>(R, ld, st, f.n, Ns, tw, lane);
-    else if (s == 0) rstage_any<T2>(R, ld, sA, f.n, Ns, tw, lane);
-    else if (s == last) { if (in_A) rstage_any<T2>(R, lA, st, f.n, Ns, tw, lane); else rstage_any<T2>(R, lB, st, f.n, Ns, tw, lane); }
-    else { if (in_A) rstage_any<T2>(R, lA, sB, f.n, Ns, tw, lane); else rstage_any<T2>(R, lB, sA, f.n, Ns, tw, lane); }
-    Ns *= R;
-  }
-}
-
-template <typename T2, int NC, bool HZ = false, class Ld, class St>
-__device__ __forceinline__ void fft_any(const FftPlan& f, Ld ld, St st, T2* A, T2* B, const T2* tw, int lane) {
-  if constexpr (NC > 0) fft_pow2<T2, NC, HZ>(ld, st, A, B, tw, lane);
-  else fft_rt<T2>(f, ld, st, A, B, tw, lane);
-}
 
 // ---------------------------------------------------------------- cp.async (LDGSTS): many loads in flight
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {

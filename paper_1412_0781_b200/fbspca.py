@@ -204,6 +204,17 @@ def fbspca_synthesize(plan: Plan, coeffs: torch.Tensor, out=None, stream=None) -
     return out
 
 
+def fbspca_estimate_params(images: torch.Tensor, fraction: float = 0.999):
+    """NEXT-2: (sigma2, R, c) of an n x L x L stack on its CUDA device (see include/fbspca.h)."""
+    n, L, L2 = images.shape
+    assert L == L2 and images.is_cuda and images.is_contiguous()
+    dt = F32 if images.dtype == torch.float32 else F64
+    s2, R, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    check(lib().fbspca_estimate_params(L, dt, images.device.index, _ptr(images), n, float(fraction), ctypes.byref(s2),
+                                       ctypes.byref(R), ctypes.byref(c)), "fbspca_estimate_params")
+    return s2.value, R.value, c.value
+
+
 def fbspca_project(plan: Plan, coeffs: torch.Tensor, mean, evals, evecs, sigma2: float = 0.0, mode: int = 0,
                    n_total: int | None = None, out=None, stream=None) -> torch.Tensor:
     n = coeffs.shape[1]

@@ -392,3 +392,20 @@ def test_denoise_pipeline_parity_c2():
     disk = (idx[:, None] ** 2 + idx[None, :] ** 2) <= cfg["R"] ** 2
     noisy = imgs[:8].cpu().numpy()
     assert np.linalg.norm((den.cpu().numpy() - clean)[:, disk]) < 0.5 * np.linalg.norm((noisy - clean)[:, disk])
+
+
+# ------------------------------------------------------------------ NEXT-2: parameter estimation
+@pytest.mark.parametrize("name,n", [("C2", 3000), ("C3", 600)])
+def test_estimate_params_parity(name, n):
+    """fbspca_estimate_params vs the oracle's estimators on the same stack: sigma^2 to 1e-9 relative (fp64 sums),
+    R and c identical (bin indices; a tie within 1e-9 of the 0.999 threshold would be reported)."""
+    cfg, imgs = blob_case(name, 0, n)
+    s2, R, c = F.fbspca_estimate_params(imgs, 0.999)
+    st = imgs.double().cpu().numpy()
+    s2_o = O.estimate_noise_variance(st)
+    assert abs(s2 - s2_o) <= 1e-9 * abs(s2_o)
+    assert R == O.estimate_support(st, s2_o, 0.999)
+    assert c == O.estimate_bandlimit(st, s2_o, 0.999)
+    # the blob model's noise level (reading Q15) is what the estimator recovers
+    sig = float(synth.blobs.noise_sigma(cfg, device=DEV))
+    assert abs(s2 - sig ** 2) <= 0.05 * sig ** 2

@@ -458,3 +458,35 @@ def test_backproject_inverts_projection():
     back = O.backproject(O.spca_coeffs(Ac, U), mean, U)
     for x, y in zip(back, a):
         assert np.allclose(x, y, atol=1e-12)
+
+
+# ---------------------------------------------------------------- NEXT-2: parameter estimation
+def test_noise_variance_white_noise_and_homogeneity():
+    """Pure white noise sigma = 3 (n = 1000, L = 64): sigma^2 within 3 % of 9 (SPEC example; P:523 "sigma^2 = 9");
+    doubling the amplitudes quadruples the estimate; constant images give 0."""
+    rng = np.random.default_rng(1)
+    st = 3.0 * rng.standard_normal((1000, 64, 64))
+    s2 = O.estimate_noise_variance(st)
+    assert abs(s2 - 9.0) <= 0.03 * 9.0
+    assert abs(O.estimate_noise_variance(2 * st) - 4 * s2) <= 1e-9 * s2
+    assert O.estimate_noise_variance(np.ones((5, 32, 32))) == 0.0
+
+
+def test_support_and_bandlimit_phantoms():
+    """Signal filling the disk of radius 20 (i.i.d. pixels inside, zero outside; negligible noise): R in [19, 22].
+    A phantom band-limited to c = 0.25 (white noise low-passed by an ideal disk filter): c in [0.23, 0.28].
+    Pure noise raises (SPEC examples)."""
+    rng = np.random.default_rng(2)
+    idx = np.arange(64) - 32
+    disk = np.hypot(*np.meshgrid(idx, idx, indexing="ij")) <= 20
+    st = rng.standard_normal((200, 64, 64)) * disk + 1e-3 * rng.standard_normal((200, 64, 64))
+    R = O.estimate_support(st, O.estimate_noise_variance(st), 0.999)
+    assert 19 <= R <= 22, R
+    L = 64
+    f = np.fft.fftfreq(L)
+    mask = np.hypot(*np.meshgrid(f, f, indexing="ij")) <= 0.25
+    band = np.real(np.fft.ifft2(np.fft.fft2(rng.standard_normal((300, L, L))) * mask))
+    c = O.estimate_bandlimit(band, 0.0, 0.999)
+    assert 0.23 <= c <= 0.28, c
+    with pytest.raises(ValueError):
+        O.estimate_support(rng.standard_normal((50, 32, 32)), 10.0, 0.999)
