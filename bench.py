@@ -343,10 +343,13 @@ def main():
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32" if dt == F.F32 else "f64", "data": "synthetic",
-            "config": {"workload": f"{cfg['name']}: BASELINE.json configs[{int(cfg['name'][1]) - 1}]", "n": n,
+            "config": {"workload": (f"{cfg['name']}: BASELINE.json configs[{int(cfg['name'][1]) - 1}]"
+                                    if cfg["name"].startswith("C") else
+                                    f"{cfg['name']}: the paper's Table III workload (P:481-501)"), "n": n,
                        "L": cfg["L"], "R": cfg["R"], "c": cfg["c"], "parallelism": f"dp{world}",
                        "n_per_rank": n_local, "eps": 1e-5, "M": plan.M, "w": plan.w,
-                       "l2": "inputs larger than L2 (6.5 GB images per step at C3)"},
+                       "l2": f"inputs larger than L2 ({n * cfg['L'] * cfg['L'] * (4 if dt == F.F32 else 8) / 1e9:.1f} GB "
+                             "of images read per step, L2 126 MB)"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
                          "frac": achieved / alu_peak, "traffic": traffic, "kernel": "polar_K1K2K3",
                          "traffic_source": "profiles/r1_ncu_traffic.json (ncu dram bytes per image x images per launch)",

@@ -31,6 +31,8 @@ CONFIGS = {
                sig=(3.0, 12.0), snr=1 / 30, rotate=False),
     "C5": dict(n=50_000, L=360, R=180.0, c=0.5, dtype="f32", model="blobs", nblobs=80,
                sig=(4.0, 16.0), snr=1 / 20, rotate=False),
+    # the paper's own timing workload (Table III): 10^5 images of N(0,1) noise, 300 x 300, R = 150, c = 1/2
+    "T3": dict(n=100_000, L=300, R=150.0, c=0.5, dtype="f32", model="noise"),
 }
 
 
@@ -41,6 +43,8 @@ def config(name: str) -> dict:
 
 
 def _clean_chunk(cfg: dict, first: int, count: int, device, seed: int) -> torch.Tensor:
+    if cfg["model"] == "noise":
+        return torch.zeros((count, cfg["L"], cfg["L"]), dtype=torch.float64, device=device)
     L, R, c, nb = cfg["L"], cfg["R"], cfg["c"], cfg["nblobs"]
     lo, hi = cfg["sig"]
     img = torch.arange(first, first + count, dtype=torch.int64, device=device)[:, None]
@@ -65,7 +69,9 @@ def _clean_chunk(cfg: dict, first: int, count: int, device, seed: int) -> torch.
 
 
 def noise_sigma(cfg: dict, device="cpu", seed: int = 0) -> float:
-    """sigma_n = sqrt(var(clean images 0..min(n,1024)-1) / SNR)  (reading Q15)."""
+    """sigma_n = sqrt(var(clean images 0..min(n,1024)-1) / SNR)  (reading Q15); 1 for pure-noise configs."""
+    if cfg["model"] == "noise":
+        return 1.0
     m = min(cfg["n"], 1024)
     parts = [_clean_chunk(cfg, s, min(CHUNK, m - s), device, seed) for s in range(0, m, CHUNK)]
     v = torch.cat(parts).var().item()

@@ -109,7 +109,7 @@ def test_expand_rotation_reflection_on_gpu():
         assert np.max(np.abs(A[k][:, 2] - np.conj(A[k][:, 0]))) <= 1e-4 * scale
 
 
-@pytest.mark.parametrize("name,n", [("C4", 2), ("C5", 1)])
+@pytest.mark.parametrize("name,n", [("C4", 2), ("C5", 1), ("T3", 1)])
 def test_expand_parity_large_L(name, n):
     cfg, imgs = blob_case(name, 0, n)
     plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=64)
