@@ -44,6 +44,7 @@ struct PolarParams {
   int smem_region_bytes;          // bytes of the shared work region (complex units * sizeof)
   int img_off;                    // complex-element offset of the staged image in the region (-1: read global)
   int img_prefetch;               // 1: the next image is loaded (cp.async) during the angular pass
+  int ring_pairs;                 // 1: n_theta = 2 M, rings transformed in pairs of M-point FFTs (K3)
   FftPlan fft_M, fft_theta;
   // device pointers (plan-owned)
   const void* deapod;             // L values (T): d(i) = 1/Phi(i/M), i = a - floor(L/2)

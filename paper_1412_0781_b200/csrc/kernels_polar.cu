@@ -347,7 +347,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
     //   odd k = 2m+1: V = DFT_N((Im f_j + i Im f_j') w^l),   ghat_j = i (V(m) + conj V(N-1-m)), ghat_j' = V(m) - conj V(N-1-m)
     // (the real-input pair trick on each parity; w^l shifts the odd frequencies onto the N-point grid).
     // Runtime sizes: one full n_theta-point FFT per ring rebuilt from the half ring.
-    T2* stg = (MC > 0) ? region : region + (size_t)pp.ang_warps * 2 * NTP;
+    T2* stg = (MC > 0 || pp.ring_pairs) ? region : region + (size_t)pp.ang_warps * 2 * NTP;
     const int GS = G | 1;                            // odd staging stride (bank spread)
     // MC = 256 (one ring pair per warp per group): the pair's first-stage inputs f[lane + 32 r], r < 8, of both
     // rings are loaded into registers one group ahead (the loads of group j0 + G fly during group j0's FFTs and
@@ -454,6 +454,44 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           for (int m = lane; 2 * m + 1 <= kmx; m += 32) {
             const T2 v = res[padi(m)];
             T2 vc = res[padi(MC - 1 - m)];
+            vc.y = -vc.y;
+            const T2 sp = cadd(v, vc), dm = csub(v, vc);
+            stg[(size_t)(2 * m + 1) * GS + jj] = T2{-sp.y, sp.x};
+            if (two) stg[(size_t)(2 * m + 1) * GS + jj + 1] = dm;
+          }
+          __syncwarp();
+        }
+      } else if (pp.ring_pairs) {
+        // runtime sizes with n_theta = 2 M: the same ring-pair scheme as above on M-point mixed-radix FFTs
+        const int kmx = pp.k_max, Mr = pp.fft_M.n;
+        T2* res = ((pp.fft_M.nstages - 1) & 1) ? myB : myA;
+        auto stR = [res](int i, T2 v) { res[padi(i)] = v; };
+        for (int pr = warp; warp < pp.fft_warps && 2 * pr < g; pr += pp.fft_warps) {
+          const int jj = 2 * pr;
+          const bool two = jj + 1 < g;
+          const T2* fa = Pol + (int64_t)(j0 + jj) * half;
+          const T2* fb = two ? fa + half : fa;
+          auto ldu = [&](int t) -> T2 { const T2 a = fa[t], b = fb[t]; return T2{a.x, two ? b.x : T(0)}; };
+          fft_rt<T2>(pp.fft_M, ldu, stR, myA, myB, twM, lane);
+          __syncwarp();
+          for (int m = lane; 2 * m <= kmx; m += 32) {
+            const T2 u = res[padi(m)];
+            T2 uc = res[padi(m == 0 ? 0 : Mr - m)];
+            uc.y = -uc.y;
+            const T2 sp = cadd(u, uc), dm = csub(u, uc);
+            stg[(size_t)(2 * m) * GS + jj] = sp;
+            if (two) stg[(size_t)(2 * m) * GS + jj + 1] = T2{dm.y, -dm.x};
+          }
+          __syncwarp();
+          auto ldv = [&](int t) -> T2 {
+            const T2 a = fa[t], b = fb[t];
+            return cmul(T2{a.y, two ? b.y : T(0)}, twT[t]);
+          };
+          fft_rt<T2>(pp.fft_M, ldv, stR, myA, myB, twM, lane);
+          __syncwarp();
+          for (int m = lane; 2 * m + 1 <= kmx; m += 32) {
+            const T2 v = res[padi(m)];
+            T2 vc = res[padi(Mr - 1 - m)];
             vc.y = -vc.y;
             const T2 sp = cadd(v, vc), dm = csub(v, vc);
             stg[(size_t)(2 * m + 1) * GS + jj] = T2{-sp.y, sp.x};

@@ -295,7 +295,10 @@ fbspca_status build_host_plan(Plan& P) {
   const int csz = (P.dt == FBSPCA_F32) ? 8 : 16;       // sizeof complex
   const int cap = polar_max_smem();
   pp.fft_warps = 16;
-  while (pp.fft_warps > 2 && pp.fft_warps * 2 * M * csz > cap / 3) pp.fft_warps /= 2;
+  // ring-pair plans (n_theta = 2 M) run K3 in the per-warp FFT scratch too, so more of the budget goes there
+  const int fft_share = (P.n_theta == 2 * M) ? 2 : 3;
+  while (pp.fft_warps > 2 && pp.fft_warps * 2 * M * csz > cap / fft_share) pp.fft_warps /= 2;
+  if (const char* e = getenv("FBSPCA_FFT_WARPS")) pp.fft_warps = std::max(1, std::min(16, atoi(e)));
   const int fixed = polar_fixed_smem(M, P.n_theta, L, csz, pp.fft_warps);
   const int budget = cap - fixed;
   const int kk = (P.k_max + 1) | 1;                    // staging row stride (odd)
@@ -319,7 +322,9 @@ fbspca_status build_host_plan(Plan& P) {
   pp.S = S;
   // pow2 plans (n_theta = 2 M, M in {64..512}) run the ring FFTs as pairs of half-length FFTs in the per-warp
   // FFT scratch (kernels_polar.cu K3): the staging [k][ring] for 32 rings is all the region holds then
-  const bool ring_pairs = P.n_theta == 2 * M && (M == 64 || M == 128 || M == 256 || M == 512);
+  const bool pow2_kernel = M == 64 || M == 128 || M == 256 || M == 512;
+  const bool ring_pairs = P.n_theta == 2 * M && !getenv("FBSPCA_NO_RT_PAIRS") ;
+  pp.ring_pairs = ring_pairs ? 1 : 0;
   if (ring_pairs) {
     Gsel = std::min(32, P.n_xi);
     while (Gsel > 2 && (Gsel | 1) * kk * csz > std::max(rows_g * S * csz, pp.fft_warps * M * csz)) Gsel /= 2;
@@ -357,7 +362,7 @@ fbspca_status build_host_plan(Plan& P) {
     const int last = std::min(phase_lo[p] + S - 1, b2max + w - 1);
     return (u2 + w <= last) ? p : -1;
   };
-  const bool doubles = P.dt == FBSPCA_F32 && w == 6 && ring_pairs && !getenv("FBSPCA_NO_DOUBLES");
+  const bool doubles = P.dt == FBSPCA_F32 && w == 6 && ring_pairs && pow2_kernel && !getenv("FBSPCA_NO_DOUBLES");
   std::vector<std::vector<std::array<int, 3>>> ph_single(phase_lo.size()), ph_double(phase_lo.size());
   std::vector<uint32_t> singles;
   std::vector<std::array<uint32_t, 2>> dbl;
