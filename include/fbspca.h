@@ -61,6 +61,7 @@ typedef enum { FBSPCA_F32 = 0, FBSPCA_F64 = 1 } fbspca_dtype;
  * table N_{k,q} J_k(R_{k,q} xi_j/c) xi_j w_j (2 pi/n_theta) (Eq. (a) P:195 with the 1/n_theta of
  * Eq. (1DFFT) P:189 folded in), and the NUFFT window (width from eps) and deapodisation.
  *   L        image side (>= 4).  c band limit in (0, 1/2].  R support radius, 2 <= R <= L/2, cR >= 1.
+ *            2L and n_theta must factor into 2, 3, 5, 7, 11, 13 and n_theta must be even, else FBSPCA_ERR_CONFIG.
  *   eps      NUFFT accuracy target (relative l2 of the polar samples), [1e-14, 1e-3]; <= 0 picks the
  *            default (1e-5 for F32, 1e-12 for F64).  F32 rejects eps < 1e-6.
  *   dt       FBSPCA_F32: images float, coefficients complex64.  FBSPCA_F64: double / complex128.
@@ -168,7 +169,7 @@ fbspca_status fbspca_synthesize(fbspca_plan_t plan, const void* d_coeffs, int64_
  *   sigma2 = mean variance over radius bins ceil(0.45 L) <= b < floor(L/2)   (the outer 10 % of radii below L/2),
  *   R      = smallest b with sum_{b' <= b} max(var_b' - sigma2, 0) b'  >= fraction x its total over b < floor(L/2),
  *   c      = b / L for the smallest frequency bin 1 <= b <= floor(L/2) with the same rule on the power spectrum.
- * d_images: n x L x L (float or double per dt) on `device`; L must be 2^a 3^b 5^c; n >= 2; 0 < fraction <= 1
+ * d_images: n x L x L (float or double per dt) on `device`; L must be 2^a 3^b 5^c 7^d 11^e 13^f; n >= 2; 0 < fraction <= 1
  * (the paper uses 0.999).  Synchronous; allocates and frees its own scratch (this is not a plan call).
  * FBSPCA_ERR_NUMERIC when no variance / power exceeds the noise level (pure noise). */
 fbspca_status fbspca_estimate_params(int L, fbspca_dtype dt, int device, const void* d_images, int64_t n,

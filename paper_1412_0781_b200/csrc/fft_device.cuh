@@ -203,7 +203,22 @@ __device__ __forceinline__ void rstage(Ld ld, St st, int N, int Ns, const T2* __
     const int jm = j % Ns;
 #pragma unroll
     for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[jm * step * r]);
-    Dft<T2, R>::run(v);
+    if constexpr (R == 7 || R == 11 || R == 13) {
+      // other prime radices (awkward n_theta = ceil(16 c R), e.g. 308 = 4 7 11): direct R-point DFT with
+      // w_R^m = tw[m N / R] from the same linear table
+      T2 o[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        T2 acc = v[0];
+#pragma unroll
+        for (int r = 1; r < R; ++r) acc = cadd(acc, cmul(v[r], tw[((q * r) % R) * (N / R)]));
+        o[q] = acc;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = o[r];
+    } else {
+      Dft<T2, R>::run(v);
+    }
     const int idxD = (j - jm) * R + jm;
 #pragma unroll
     for (int r = 0; r < R; ++r) st(idxD + r * Ns, v[r]);
@@ -218,6 +233,9 @@ __device__ __forceinline__ void rstage_any(int R, Ld ld, St st, int N, int Ns, c
     case 4: rstage<T2, 4>(ld, st, N, Ns, tw, lane); break;
     case 2: rstage<T2, 2>(ld, st, N, Ns, tw, lane); break;
     case 5: rstage<T2, 5>(ld, st, N, Ns, tw, lane); break;
+    case 7: rstage<T2, 7>(ld, st, N, Ns, tw, lane); break;
+    case 11: rstage<T2, 11>(ld, st, N, Ns, tw, lane); break;
+    case 13: rstage<T2, 13>(ld, st, N, Ns, tw, lane); break;
     default: rstage<T2, 3>(ld, st, N, Ns, tw, lane); break;
   }
 }

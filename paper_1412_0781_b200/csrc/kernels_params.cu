@@ -140,7 +140,9 @@ static fbspca_status estimate_t(int L, int device, const T* d_img, int64_t n, do
     while (m % 2 == 0 && fp.nstages < kMaxRadixStages) push(2);
     while (m % 5 == 0 && fp.nstages < kMaxRadixStages) push(5);
     while (m % 3 == 0 && fp.nstages < kMaxRadixStages) push(3);
-    if (m != 1) { set_error("estimate_params: L must be 2^a 3^b 5^c"); return FBSPCA_ERR_CONFIG; }
+    for (int r : {7, 11, 13})
+      while (m % r == 0 && fp.nstages < kMaxRadixStages) push(r);
+    if (m != 1) { set_error("estimate_params: L must be 2^a 3^b 5^c 7^d 11^e 13^f"); return FBSPCA_ERR_CONFIG; }
   }
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);

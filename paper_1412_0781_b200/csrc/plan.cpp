@@ -102,6 +102,8 @@ FftPlan make_fft(int n) {
   while (m % 2 == 0 && f.nstages < kMaxRadixStages) push(2);
   while (m % 5 == 0 && f.nstages < kMaxRadixStages) push(5);
   while (m % 3 == 0 && f.nstages < kMaxRadixStages) push(3);
+  for (int r : {7, 11, 13})
+    while (m % r == 0 && f.nstages < kMaxRadixStages) push(r);
   if (m != 1) f.nstages = -1;
   return f;
 }
@@ -290,7 +292,7 @@ fbspca_status build_host_plan(Plan& P) {
   pp.col_lo = b2min; pp.ncols_x = b2max + w - b2min;
   pp.beta = P.beta; pp.half_w = hw;
   pp.fft_M = make_fft(M); pp.fft_theta = make_fft(P.n_theta);
-  if (pp.fft_M.nstages < 0 || pp.fft_theta.nstages < 0) { set_error("FFT sizes must be 2^a 3^b 5^c"); return FBSPCA_ERR_CONFIG; }
+  if (pp.fft_M.nstages < 0 || pp.fft_theta.nstages < 0) { set_error("FFT sizes must be 2^a 3^b 5^c 7^d 11^e 13^f"); return FBSPCA_ERR_CONFIG; }
   pp.nwarps = 16;
   const int csz = (P.dt == FBSPCA_F32) ? 8 : 16;       // sizeof complex
   const int cap = polar_max_smem();

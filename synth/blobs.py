@@ -33,6 +33,11 @@ CONFIGS = {
                sig=(4.0, 16.0), snr=1 / 20, rotate=False),
     # the paper's own timing workload (Table III): 10^5 images of N(0,1) noise, 300 x 300, R = 150, c = 1/2
     "T3": dict(n=100_000, L=300, R=150.0, c=0.5, dtype="f32", model="noise"),
+    # the paper's ribosome experiment shape: 10^5 images of 240 x 240, R = 98, c = 0.196,
+    # SNR 1/30 -- n_theta = ceil(16 c R) = 308 = 4 7 11 (radix-7/11 angular FFTs); synthetic blobs stand in for
+    # the EMDB-2762 projections (dataset absent)
+    "RB": dict(n=100_000, L=240, R=98.0, c=0.196, dtype="f32", model="blobs", nblobs=50,
+               sig=(3.0, 12.0), snr=1 / 30, rotate=False),
 }
 
 

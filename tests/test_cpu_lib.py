@@ -48,6 +48,22 @@ def test_host_plan_matches_oracle(L, R):
     assert pl.n_theta % 2 == 0 and pl.M >= 2 * L
 
 
+@pytest.mark.parametrize("L,c,R", [(240, 0.196, 98.0), (100, 0.3, 40.0)])
+def test_host_plan_general_c(L, c, R):
+    """c < 1/2 (the ribosome shape P:536: n_theta = ceil(16 c R) = 308 = 4 7 11, radix-7/11 angular FFTs)."""
+    pl = F.fbspca_plan(L, c, R, device=-1)
+    b = O.build_basis(c, R)
+    assert pl.k_max == b.k_max and np.array_equal(pl.p, b.p)
+    assert pl.n_xi == b.n_xi and pl.n_theta == b.n_theta
+    xo, wo, _ = O.polar_grid(b)
+    assert np.max(np.abs(pl.xi - xo)) < 1e-15
+
+
+def test_plan_fft_size_error():
+    with pytest.raises(FbspcaError, match="CONFIG"):       # n_theta = ceil(16 * 0.5 * 4.25) = 34 = 2 17
+        F.fbspca_plan(16, 0.5, 4.25, device=-1)
+
+
 def test_plan_window_and_phases():
     pl = F.fbspca_plan(128, 0.5, 64, device=-1)
     assert pl.w == 6 and abs(pl.beta - float(np.float32(2.3 * 6))) < 1e-12   # fp32 plans round beta to float (DESIGN Q16) and pl.M == 256

@@ -109,7 +109,7 @@ def test_expand_rotation_reflection_on_gpu():
         assert np.max(np.abs(A[k][:, 2] - np.conj(A[k][:, 0]))) <= 1e-4 * scale
 
 
-@pytest.mark.parametrize("name,n", [("C4", 2), ("C5", 1), ("T3", 1)])
+@pytest.mark.parametrize("name,n", [("C4", 2), ("C5", 1), ("T3", 1), ("RB", 2)])
 def test_expand_parity_large_L(name, n):
     cfg, imgs = blob_case(name, 0, n)
     plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=64)
@@ -302,7 +302,7 @@ def test_c3_full_size_spectral_parity():
     _spectral_checks(plan, blocks, mean, evals, evecs, m_o, C_o)
 
 
-@pytest.mark.parametrize("name,n", [("C4", 2048), ("C5", 1024)])
+@pytest.mark.parametrize("name,n", [("C4", 2048), ("C5", 1024), ("RB", 2048)])
 def test_large_L_spectral_parity_subset(name, n):
     """configs[3] (L = 256, pow2 kernels, R = 128 tensor-core covariance) and configs[4] (L = 360, runtime
     mixed-radix FFTs, p_k up to 179): a subset of images through K1-K6, oracle K5/K6 on the GPU coefficients."""
