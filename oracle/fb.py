@@ -22,7 +22,7 @@ __all__ = [
     "radial_table", "polar_ft_direct", "angular_transform", "radial_quadrature",
     "expand", "expand_polar", "synthesize_polar", "mean_and_center",
     "block_covariance", "covariance_partials", "finalize_covariance",
-    "block_eig", "sign_normalize", "radial_eigenfunctions", "spca_coeffs", "mp_edge", "mp_select",
+    "block_eig", "svd_route", "sign_normalize", "radial_eigenfunctions", "spca_coeffs", "mp_edge", "mp_select",
     "shrink_weights", "project", "backproject", "synthesize_pixels", "rotate_coeffs", "reflect_coeffs",
     "flat_index", "to_flat", "from_flat",
     "radial_profile", "estimate_noise_variance", "estimate_support", "estimate_bandlimit",
@@ -287,6 +287,29 @@ def block_eig(C: list):
         lam.append(w[o])
         U.append(sign_normalize(V[:, o]))
     return lam, U
+
+
+def svd_route(A: list):
+    """Alg. 2 line 4, SVD form ("or perform SVD of A^(k) and take the left singular
+    vectors", the route for n < p_k).  B_k = [Re A_k, Im A_k] / sqrt(n) (k = 0: A_0 minus the mean, real)
+    has B_k B_k^T = C^(k) of Eqs. (ck)/(ck_0), so lambda = s^2 and U = left singular vectors
+    (numpy.linalg.svd, full_matrices: a complete basis when rank < p_k; zero singular values appended).
+    Returns (mean, lam, U) like covariance + block_eig."""
+    n = A[0].shape[1]
+    mean = A[0].real.mean(axis=1)
+    lam, U = [], []
+    for k, Ak in enumerate(A):
+        if k == 0:
+            B = (Ak.real - mean[:, None]) / math.sqrt(n)
+        else:
+            B = np.concatenate([Ak.real, Ak.imag], axis=1) / math.sqrt(n)
+        Uk, sv, _ = np.linalg.svd(B, full_matrices=True)
+        lk = np.zeros(B.shape[0])
+        lk[: sv.size] = sv ** 2
+        o = np.argsort(-lk, kind="stable")
+        lam.append(lk[o])
+        U.append(sign_normalize(Uk[:, o]))
+    return mean, lam, U
 
 
 def radial_eigenfunctions(basis: Basis, U: list, xi=None) -> list:

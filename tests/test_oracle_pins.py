@@ -331,6 +331,29 @@ def test_eig_matches_svd_route_and_sign_convention():
             assert Uk[q, l] > 0
 
 
+@pytest.mark.parametrize("n", [1, 4, 9])
+def test_svd_route_rank_deficient(n):
+    """O.svd_route (n < p_k): the eigenpairs of C^(k) (Eqs. (ck)/(ck_0)) from the SVD of A_k, with a
+    complete basis and exactly p_k - rank zero eigenvalues (rank 2n for k >= 1, n - 1 for the centred k = 0)."""
+    b = O.build_basis(0.5, 16)
+    A = _random_A(b, n, 11)
+    mean_c, C = O.block_covariance(A)
+    lam_e, _ = O.block_eig(C)
+    mean, lam, U = O.svd_route(A)
+    assert np.allclose(mean, mean_c, atol=1e-15)
+    for k, (lk, le, Uk, Ck) in enumerate(zip(lam, lam_e, U, C)):
+        pk = b.p[k]
+        scale = max(1.0, le.max())
+        assert np.allclose(lk, le, atol=1e-12 * scale)
+        rank = min(pk, n - 1 if k == 0 else 2 * n)
+        assert np.all(lk[:rank] > 1e-8 * scale) and np.all(np.abs(lk[rank:]) <= 1e-12 * scale)
+        assert np.allclose(Uk.T @ Uk, np.eye(pk), atol=1e-12)
+        assert np.allclose(Ck @ Uk, Uk * lk[None, :], atol=1e-11 * scale)
+        for l in range(pk):
+            q = np.argmax(np.abs(Uk[:, l]))
+            assert Uk[q, l] > 0
+
+
 def test_projection_properties():
     b = O.build_basis(0.5, 8)
     n = 30
