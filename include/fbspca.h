@@ -7,6 +7,7 @@
  *   Algorithm 1  fbspca_expand      images -> FB coefficients a_{k,q}
  *   Algorithm 2  fbspca_covariance  C^(k) = Re(A_k A_k^*)/n, mean at k=0 only
  *                            fbspca_eig         C^(k) = U_k diag(lambda^(k)) U_k^T
+ *                            fbspca_svd         the same eigenpairs from the SVD of A_k (n < p_k)
  *                            fbspca_radial_eigenfunctions  f^{k,l}(xi_j) (Alg. 2 line 5)
  *   NEXT-1 (denoising)       fbspca_backproject  a_k = U_k c_k (+ mean): filtered steerable coefficients -> FB
  *                            fbspca_synthesize   FB coefficients -> pixel images (Eq. (IFT_FB))
@@ -127,6 +128,20 @@ fbspca_status fbspca_allreduce_partial(fbspca_plan_t plan, double* d_partial, vo
  * Synchronises the stream to check convergence (<= 30 sweeps); FBSPCA_ERR_NUMERIC names the block. */
 fbspca_status fbspca_eig(fbspca_plan_t plan, const double* d_blocks, double* d_evals, double* d_evecs,
                          fbspca_stream_t stream);
+
+/* Alg. 2 line 4, SVD form ("or perform SVD of A^(k) and take the left singular vectors";
+ * the route for n < p_k), fp64, one CTA per block: the left singular vectors and squared singular values of
+ * the real p_k x 2n matrix [Re A_k, Im A_k] / sqrt(n) (k = 0: A_0 - mean 1^T, Im taken as 0), i.e. the eigenpairs
+ * of C^(k) = Re(A_k A_k^*)/n without forming C^(k), by one-sided (Hestenes) Jacobi.  Output in fbspca_eig's
+ * layout, order and sign convention; U_k is complete (orthonormal p_k x p_k) when rank < p_k, with the zero
+ * singular values last.
+ *   d_coeffs  coefficient layout, ld = n (all the images: the route is single-device).  n >= 1.
+ *   d_mean    p_0 doubles receiving the k = 0 mean, or NULL.
+ *   Cost O(sweeps p_k^2 (n + p_k)) per block; workspace (2 n sum_k p_k + sum_k p_k^2 doubles) is allocated
+ *   and freed stream-ordered inside the call.  Synchronises the stream to check convergence (<= 40 sweeps;
+ *   FBSPCA_ERR_NUMERIC names the block).  For large n use fbspca_covariance + fbspca_eig. */
+fbspca_status fbspca_svd(fbspca_plan_t plan, const void* d_coeffs, int64_t n, double* d_mean, double* d_evals,
+                         double* d_evecs, fbspca_stream_t stream);
 
 /* Alg. 2 line 5, Eq. (sPCArad): the radial eigenfunctions at the plan's GL nodes xi_j,
  *   f^{k,l}(xi_j) = sum_q u_l^(k)(q) N_{k,q} J_k(R_{k,q} xi_j / c),   fp64.

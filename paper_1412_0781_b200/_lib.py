@@ -30,6 +30,7 @@ SIGNATURES = {
     "fbspca_covariance_accumulate": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "fbspca_allreduce_partial": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "fbspca_eig": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "fbspca_svd": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "fbspca_radial_eigenfunctions": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "fbspca_backproject": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "fbspca_synthesize": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),

@@ -391,6 +391,41 @@ fbspca_status fbspca_eig(fbspca_plan_t h, const double* d_blocks, double* d_eval
   return FBSPCA_OK;
 }
 
+fbspca_status fbspca_svd(fbspca_plan_t h, const void* d_coeffs, int64_t n, double* d_mean, double* d_evals,
+                         double* d_evecs, fbspca_stream_t stream) {
+  fbspca_status st = check_compute_plan(h);
+  if (st != FBSPCA_OK) return st;
+  Plan& P = *h;
+  if (!d_coeffs || !d_evals || !d_evecs || n < 1) { set_error("svd: bad argument"); return FBSPCA_ERR_ARG; }
+  if (!aligned(d_coeffs, P.dt == FBSPCA_F32 ? 8 : 16) || !aligned(d_evals, 8) || !aligned(d_evecs, 8) ||
+      (d_mean && !aligned(d_mean, 8))) { set_error("svd: misaligned pointer"); return FBSPCA_ERR_ARG; }
+  if (P.p[0] > kSvdMaxP) { set_error("svd: p_0 above the kernel's bound"); return FBSPCA_ERR_CONFIG; }
+  DeviceGuard g(P.device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t ncoef = P.coef_off[P.k_max + 1];
+  const size_t bytes = (size_t)(2 * n * ncoef + P.evec_off[P.k_max + 1]) * sizeof(double);
+  double* work = nullptr;
+  FB_CUDA(cudaMallocAsync(&work, bytes, s), "svd workspace");
+  cudaError_t e;
+  {
+    TimedRegion t(P, T_EIG, s);
+    e = launch_svd(P, d_coeffs, n, work, d_mean, d_evals, d_evecs, s);
+  }
+  cudaFreeAsync(work, s);
+  FB_CUDA(e, "svd kernel");
+  std::vector<int> sweeps(P.k_max + 1);
+  FB_CUDA(cudaMemcpyAsync(sweeps.data(), P.d_eig_sweeps, sweeps.size() * sizeof(int), cudaMemcpyDeviceToHost, s),
+          "svd sweeps");
+  FB_CUDA(cudaStreamSynchronize(s), "svd sync");
+  for (int k = 0; k <= P.k_max; ++k)
+    if (sweeps[k] >= kSvdMaxSweeps) {
+      set_error("one-sided Jacobi did not converge within " + std::to_string(kSvdMaxSweeps) + " sweeps for block k = " +
+                std::to_string(k));
+      return FBSPCA_ERR_NUMERIC;
+    }
+  return FBSPCA_OK;
+}
+
 fbspca_status fbspca_radial_eigenfunctions(fbspca_plan_t h, const double* d_evecs, double* d_f,
                                            fbspca_stream_t stream) {
   fbspca_status st = check_compute_plan(h);

@@ -151,6 +151,10 @@ cudaError_t launch_cov_accum(const Plan& P, const void* d_coeffs, int64_t ld, in
                              double* d_partial, cudaStream_t s);
 cudaError_t launch_cov_finalize(const Plan& P, const double* d_partial, double* d_blocks, double* d_mean,
                                 cudaStream_t s);
+constexpr int kSvdMaxP = 1024;          // p_k bound of the SVD route's shared mean / norm scratch
+constexpr int kSvdMaxSweeps = 40;
+cudaError_t launch_svd(const Plan& P, const void* d_coeffs, int64_t n, double* d_work, double* d_mean,
+                       double* d_evals, double* d_evecs, cudaStream_t s);
 cudaError_t launch_eig(const Plan& P, const double* d_blocks, double* d_evals, double* d_evecs,
                        cudaStream_t s);
 cudaError_t launch_radial_eigfun(const Plan& P, const double* d_evecs, double* d_f, cudaStream_t s);

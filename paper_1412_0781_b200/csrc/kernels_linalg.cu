@@ -374,6 +374,139 @@ cudaError_t launch_eig(const Plan& P, const double* d_blocks, double* d_evals, d
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- Alg. 2 line 4, SVD form
+// "or perform SVD of A^(k) and take the left singular vectors" -- the route for n < p_k.  Per block k the real
+// p_k x m matrix W = [Re A_k, Im A_k] / sqrt(n) (m = 2n; k = 0: A_0 - mean 1^T with Im = 0, reading Q8) has
+// W W^T = C^(k), so its left singular vectors / squared singular values are the eigenpairs of C^(k).  One-sided
+// (Hestenes) Jacobi on the ROWS of W: rotate row pairs (p, q) until mutually orthogonal, accumulating U <- U J;
+// then W = U diag(sigma) V^T with sigma_l^2 = |w_l|^2.  U is a product of rotations, so it is a complete
+// orthonormal basis even when rank W = min(p_k, m) < p_k (the zero singular values).  One CTA per block, one warp
+// per row pair of a round-robin round (the pairs of a round are disjoint), each pair's dot products reduced in a
+// fixed order by one warp (deterministic).  The coefficient rows are contiguous (re, im interleaved): a column
+// permutation of W, which leaves every row dot product unchanged.  W and U live in a per-call global workspace
+// (L2-resident at the sizes this route is for).
+template <typename T>
+__global__ void __launch_bounds__(256)
+svd_kernel(const T* __restrict__ coeffs, int64_t n, const int* __restrict__ p, const int64_t* __restrict__ coef_off,
+           const int64_t* __restrict__ evec_off, double* __restrict__ work, double* __restrict__ mean_out,
+           double* __restrict__ evals, double* __restrict__ evecs, int* __restrict__ sweeps_out) {
+  __shared__ double smean[kSvdMaxP];
+  __shared__ int rotated;
+  const int k = blockIdx.x, pk = p[k];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int64_t m = 2 * n;
+  double* W = work + 2 * n * coef_off[k] + evec_off[k];     // p_k x m, then U (p_k x p_k)
+  double* U = W + (int64_t)pk * m;
+  const T* A = coeffs + 2 * n * coef_off[k];
+  const double isn = 1.0 / sqrt(double(n));
+  if (k == 0) {
+    for (int q = warp; q < pk; q += nw) {
+      double sacc = 0.0;
+      for (int64_t i = lane; i < n; i += 32) sacc += double(A[(int64_t)q * m + 2 * i]);
+      for (int o = 16; o > 0; o >>= 1) sacc += __shfl_down_sync(0xffffffffu, sacc, o);
+      if (lane == 0) { smean[q] = sacc / double(n); if (mean_out) mean_out[q] = sacc / double(n); }
+    }
+    __syncthreads();
+  }
+  for (int64_t e = tid; e < (int64_t)pk * m; e += blockDim.x) {
+    const int q = int(e / m);
+    const int64_t j = e - (int64_t)q * m;
+    double v = double(A[e]);
+    if (k == 0) v = (j & 1) ? 0.0 : v - smean[q];
+    W[e] = v * isn;
+  }
+  for (int e = tid; e < pk * pk; e += blockDim.x) U[e] = (e / pk == e % pk) ? 1.0 : 0.0;
+  // trace(W W^T) (rotation invariant): pairs with |w_p . w_q| <= 1e-28 tr are taken as orthogonal, so rows in
+  // the numerical null space (|w|^2 ~ eps^2 tr when rank < p_k) stop rotating
+  if (warp == 0) {
+    double acc = 0;
+    for (int64_t e = lane; e < (int64_t)pk * m; e += 32) acc = fma(W[e], W[e], acc);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if (lane == 0) smean[kSvdMaxP - 1] = acc;
+  }
+  __syncthreads();
+  const double floor_g = 1e-28 * smean[kSvdMaxP - 1];
+  const int np = pk + (pk & 1);
+  int sweep = 0;
+  for (; sweep < kSvdMaxSweeps && pk > 1; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int round = 0; round < np - 1; ++round) {
+      for (int i = warp; i < np / 2; i += nw) {
+        auto pos = [&](int t) { return t == 0 ? 0 : 1 + (t - 1 + round) % (np - 1); };
+        const int a = pos(i), b = pos(np - 1 - i);
+        const int pp = min(a, b), qq = max(a, b);
+        if (qq >= pk) continue;
+        double* wp = W + (int64_t)pp * m;
+        double* wq = W + (int64_t)qq * m;
+        double al = 0, be = 0, ga = 0;
+        for (int64_t j = lane; j < m; j += 32) {
+          const double x = wp[j], y = wq[j];
+          al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          al += __shfl_down_sync(0xffffffffu, al, o);
+          be += __shfl_down_sync(0xffffffffu, be, o);
+          ga += __shfl_down_sync(0xffffffffu, ga, o);
+        }
+        al = __shfl_sync(0xffffffffu, al, 0); be = __shfl_sync(0xffffffffu, be, 0); ga = __shfl_sync(0xffffffffu, ga, 0);
+        if (!(fabs(ga) > 1e-15 * sqrt(al * be)) || !(fabs(ga) > floor_g) || fabs(ga) < 1e-300) continue;
+        const double zeta = (be - al) / (2 * ga);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
+        const double c = 1 / sqrt(1 + t * t), s = t * c;
+        for (int64_t j = lane; j < m; j += 32) {
+          const double x = wp[j], y = wq[j];
+          wp[j] = c * x - s * y; wq[j] = s * x + c * y;
+        }
+        for (int r = lane; r < pk; r += 32) {
+          const double x = U[r * pk + pp], y = U[r * pk + qq];
+          U[r * pk + pp] = c * x - s * y; U[r * pk + qq] = s * x + c * y;
+        }
+        if (lane == 0) rotated = 1;
+      }
+      __syncthreads();
+    }
+    const int any = rotated;
+    __syncthreads();
+    if (!any) break;
+  }
+  if (tid == 0) sweeps_out[k] = (pk > 1) ? sweep : 0;
+  // sigma_l^2 = |w_l|^2 (smean reused as scratch), then sort / sign as fbspca_eig (reading Q10)
+  for (int q = warp; q < pk; q += nw) {
+    const double* wq = W + (int64_t)q * m;
+    double acc = 0;
+    for (int64_t j = lane; j < m; j += 32) acc = fma(wq[j], wq[j], acc);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if (lane == 0) smean[q] = acc;
+  }
+  __syncthreads();
+  for (int i = tid; i < pk; i += blockDim.x) {
+    const double li = smean[i];
+    int rank = 0;
+    for (int j = 0; j < pk; ++j) {
+      const double lj = smean[j];
+      rank += (lj > li) || (lj == li && j < i);
+    }
+    evals[coef_off[k] + rank] = li;
+    int arg = 0; double best = -1;
+    for (int r = 0; r < pk; ++r) { const double a = fabs(U[r * pk + i]); if (a > best) { best = a; arg = r; } }
+    const double sg = U[arg * pk + i] < 0 ? -1.0 : 1.0;
+    double* Uo = evecs + evec_off[k];
+    for (int r = 0; r < pk; ++r) Uo[r * pk + rank] = sg * U[r * pk + i];
+  }
+}
+
+cudaError_t launch_svd(const Plan& P, const void* d_coeffs, int64_t n, double* d_work, double* d_mean,
+                       double* d_evals, double* d_evecs, cudaStream_t s) {
+  if (P.dt == FBSPCA_F32)
+    svd_kernel<float><<<P.k_max + 1, 256, 0, s>>>(static_cast<const float*>(d_coeffs), n, P.d_p, P.d_coef_off,
+                                                   P.d_evec_off, d_work, d_mean, d_evals, d_evecs, P.d_eig_sweeps);
+  else
+    svd_kernel<double><<<P.k_max + 1, 256, 0, s>>>(static_cast<const double*>(d_coeffs), n, P.d_p, P.d_coef_off,
+                                                    P.d_evec_off, d_work, d_mean, d_evals, d_evecs, P.d_eig_sweeps);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- Alg. 2 line 5: Eq. (sPCArad)
 // f^{k,l}(xi_j) = sum_q u_l^(k)(q) N_{k,q} J_k(R_{k,q} xi_j / c)  (fp64), one CTA per k (U_k and the basis read
 // through L1/L2: p_k^2 <= 179^2 doubles does not always fit shared memory; the step is O(sum p_k^2 n_xi), tiny).

@@ -175,6 +175,17 @@ def fbspca_eig(plan: Plan, blocks: torch.Tensor, stream=None):
     return evals, evecs
 
 
+def fbspca_svd(plan: Plan, coeffs: torch.Tensor, stream=None):
+    """Alg. 2 line 4 via the SVD of A_k (the n < p_k route): (evals, evecs, mean) as fbspca_eig."""
+    n = coeffs.shape[1]
+    evals = torch.empty(plan.n_coef, dtype=torch.float64, device=coeffs.device)
+    evecs = torch.empty(int(plan.evec_off[-1]), dtype=torch.float64, device=coeffs.device)
+    mean = torch.empty(int(plan.p[0]), dtype=torch.float64, device=coeffs.device)
+    check(lib().fbspca_svd(ctypes.c_void_p(plan.handle), _ptr(coeffs), n, _ptr(mean), _ptr(evals), _ptr(evecs),
+                           _stream_ptr(stream)), "fbspca_svd")
+    return evals, evecs, mean
+
+
 def fbspca_radial_eigenfunctions(plan: Plan, evecs: torch.Tensor, stream=None) -> torch.Tensor:
     """Alg. 2 line 5: f^{k,l}(xi_j) as a (sum_k p_k) x n_xi fp64 tensor (row coef_off[k] + l)."""
     f = torch.empty((plan.n_coef, plan.n_xi), dtype=torch.float64, device=evecs.device)

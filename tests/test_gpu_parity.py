@@ -409,3 +409,55 @@ def test_estimate_params_parity(name, n):
     # the blob model's noise level (reading Q15) is what the estimator recovers
     sig = float(synth.blobs.noise_sigma(cfg, device=DEV))
     assert abs(s2 - sig ** 2) <= 0.05 * sig ** 2
+
+
+# ------------------------------------------------------------------ SVD route (Alg. 2 line 4)
+@pytest.mark.parametrize("name,n", [("C1", 1), ("C1", 5), ("C2", 8), ("C2", 40), ("C3", 24), ("RB", 16)])
+def test_svd_route_parity(name, n):
+    """fbspca_svd vs O.svd_route on the same (GPU-expanded) coefficients: eigenvalues, mean, eigenvectors of
+    simple eigenvalues, and a complete orthonormal basis with C^(k) U = U Lambda on the null space too."""
+    if name == "C1":
+        cfg, imgs = synth.config("C1"), torch.from_numpy(synth.c1_images(n)).to(DEV)
+    else:
+        cfg, imgs = blob_case(name, 0, n)
+    dt = F.F64 if cfg["dtype"] == "f64" else F.F32
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], dtype=dt, device=0, max_batch=64)
+    coeffs = F.fbspca_expand(plan, imgs)
+    evals, evecs, mean = F.fbspca_svd(plan, coeffs)
+    torch.cuda.synchronize()
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    A = O.from_flat(coeffs.cpu().numpy().astype(np.complex128), basis)
+    m_o, lam_o, U_o = O.svd_route(A)
+    _, C_o = O.block_covariance(A)
+    ev, vv = evals.cpu().numpy(), evecs.cpu().numpy()
+    assert np.max(np.abs(mean.cpu().numpy() - m_o)) <= 1e-12 * max(1.0, np.abs(m_o).max())
+    for k in range(basis.k_max + 1):
+        pk = basis.p[k]
+        lg = ev[plan.coef_off[k]:plan.coef_off[k] + pk]
+        Ug = vv[plan.evec_off[k]:plan.evec_off[k] + pk * pk].reshape(pk, pk)
+        scale = max(lam_o[k].max(), 1e-300)
+        assert np.max(np.abs(lg - lam_o[k])) <= 1e-10 * scale, f"k={k}"
+        assert np.max(np.abs(Ug.T @ Ug - np.eye(pk))) <= 1e-11, f"k={k}"
+        assert np.max(np.abs(C_o[k] @ Ug - Ug * lg[None, :])) <= 1e-9 * scale, f"k={k}"
+        for l in range(pk):
+            gap = min([abs(lam_o[k][l] - lam_o[k][j]) for j in range(pk) if j != l] + [np.inf])
+            if lam_o[k][l] > 1e-6 * scale and gap > 1e-4 * scale:
+                assert np.max(np.abs(Ug[:, l] - U_o[k][:, l])) <= 1e-6, f"k={k} l={l}"
+
+
+def test_svd_route_matches_eig_route():
+    """n > p_k: fbspca_svd and fbspca_covariance + fbspca_eig give the same eigenvalues (C2, 200 images), to the
+    covariance kernels' accuracy."""
+    cfg, imgs = blob_case("C2", 0, 200)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=256)
+    coeffs = F.fbspca_expand(plan, imgs)
+    ev_s, _, mean_s = F.fbspca_svd(plan, coeffs)
+    blocks, mean = F.fbspca_covariance(plan, coeffs)
+    ev_e, _ = F.fbspca_eig(plan, blocks)
+    torch.cuda.synchronize()
+    a, b = ev_s.cpu().numpy(), ev_e.cpu().numpy()
+    for k in range(plan.k_max + 1):
+        sl = slice(plan.coef_off[k], plan.coef_off[k + 1])
+        # the covariance route runs k >= 1 on tcgen05 3xTF32 (about 1e-6 relative, DESIGN.md K5)
+        assert np.max(np.abs(a[sl] - b[sl])) <= 1e-5 * max(b[sl].max(), 1e-300)
+    assert torch.allclose(mean_s, mean.to(torch.float64), rtol=0, atol=1e-12)
