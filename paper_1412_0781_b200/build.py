@@ -7,8 +7,9 @@ import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-SRC = ["csrc/plan.cpp", "csrc/kernels_polar.cu", "csrc/kernels_linalg.cu", "csrc/kernels_tma.cu", "csrc/kernels_synth.cu", "csrc/kernels_params.cu", "csrc/capi.cu"]
-HDR = ["csrc/internal.h", "csrc/fft_device.cuh", os.path.join("..", "include", "fbspca.h")]
+SRC = (["csrc/plan.cpp", "csrc/kernels_polar.cu"] + [f"csrc/polar_part{i}.cu" for i in range(1, 6)] +
+       ["csrc/kernels_linalg.cu", "csrc/kernels_tma.cu", "csrc/kernels_synth.cu", "csrc/kernels_params.cu", "csrc/capi.cu"])
+HDR = ["csrc/internal.h", "csrc/fft_device.cuh", "csrc/kernels_polar.cu", os.path.join("..", "include", "fbspca.h")]
 LIB = os.path.join(PKG, "lib", "libfbspca.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",

@@ -203,15 +203,14 @@ __device__ __forceinline__ void rstage(Ld ld, St st, int N, int Ns, const T2* __
     const int jm = j % Ns;
 #pragma unroll
     for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[jm * step * r]);
-    if constexpr (R == 7 || R == 11 || R == 13) {
-      // other prime radices (awkward n_theta = ceil(16 c R), e.g. 308 = 4 7 11): direct R-point DFT with
-      // w_R^m = tw[m N / R] from the same linear table
+    if constexpr (R == 7 || R == 11) {
+      // unrolled prime DFT, w_R^m = tw[m N / R] (only the angular FFT instantiates these: see fft_rt PRIMES)
       T2 o[R];
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         T2 acc = v[0];
 #pragma unroll
-        for (int r = 1; r < R; ++r) acc = cadd(acc, cmul(v[r], tw[((q * r) % R) * (N / R)]));
+        for (int r = 1; r < R; ++r) acc = cadd(acc, cmul(v[r], tw[((q * r) % R) * NB]));
         o[q] = acc;
       }
 #pragma unroll
@@ -226,21 +225,46 @@ __device__ __forceinline__ void rstage(Ld ld, St st, int N, int Ns, const T2* __
   __syncwarp();
 }
 
+// Other prime radices (awkward n_theta = ceil(16 c R), e.g. 308 = 4 7 11, or 2L with such a factor): a direct
+// R-point DFT per butterfly, out[q] = sum_r in[r] w^(jm step r) w_R^(q r) with both factors from the same linear
+// table (w_R^m = tw[m N / R]), loops not unrolled -- O(R) loads per output, kept compact because these sizes are rare.
 template <typename T2, class Ld, class St>
+__device__ void rstage_prime(int R, Ld ld, St st, int N, int Ns, const T2* __restrict__ tw, int lane) {
+  const int NB = N / R, step = N / (Ns * R);
+  for (int j = lane; j < NB; j += 32) {
+    const int jm = j % Ns, idxD = (j - jm) * R + jm;
+#pragma unroll 1
+    for (int q = 0; q < R; ++q) {
+      T2 acc = ld(j);
+#pragma unroll 1
+      for (int r = 1; r < R; ++r) acc = cadd(acc, cmul(ld(j + r * NB), tw[(jm * step * r + ((q * r) % R) * NB) % N]));
+      st(idxD + q * Ns, acc);
+    }
+  }
+  __syncwarp();
+}
+
+template <typename T2, bool PRIMES = false, class Ld, class St>
 __device__ __forceinline__ void rstage_any(int R, Ld ld, St st, int N, int Ns, const T2* tw, int lane) {
   switch (R) {
     case 8: rstage<T2, 8>(ld, st, N, Ns, tw, lane); break;
     case 4: rstage<T2, 4>(ld, st, N, Ns, tw, lane); break;
     case 2: rstage<T2, 2>(ld, st, N, Ns, tw, lane); break;
     case 5: rstage<T2, 5>(ld, st, N, Ns, tw, lane); break;
-    case 7: rstage<T2, 7>(ld, st, N, Ns, tw, lane); break;
-    case 11: rstage<T2, 11>(ld, st, N, Ns, tw, lane); break;
-    case 13: rstage<T2, 13>(ld, st, N, Ns, tw, lane); break;
+    case 7:
+      if constexpr (PRIMES) rstage<T2, 7>(ld, st, N, Ns, tw, lane); else rstage_prime<T2>(R, ld, st, N, Ns, tw, lane);
+      break;
+    case 11:
+      if constexpr (PRIMES) rstage<T2, 11>(ld, st, N, Ns, tw, lane); else rstage_prime<T2>(R, ld, st, N, Ns, tw, lane);
+      break;
+    case 13: rstage_prime<T2>(R, ld, st, N, Ns, tw, lane); break;
     default: rstage<T2, 3>(ld, st, N, Ns, tw, lane); break;
   }
 }
 
-template <typename T2, class Ld, class St>
+// PRIMES: radix-7/11 stages unrolled (the angular FFT, where n_theta = ceil(16 c R) brings such factors); other
+// call sites use the compact rstage_prime, which keeps their code (and the build) small.
+template <typename T2, bool PRIMES = false, class Ld, class St>
 __device__ void fft_rt(const FftPlan& f, Ld ld, St st, T2* A, T2* B, const T2* tw, int lane) {
   auto lA = [A](int i) { return A[padi(i)]; };
   auto lB = [B](int i) { return B[padi(i)]; };
@@ -251,10 +275,10 @@ __device__ void fft_rt(const FftPlan& f, Ld ld, St st, T2* A, T2* B, const T2* t
   for (int s = 0; s <= last; ++s) {
     const int R = f.radix[s];
     const bool in_A = (s & 1);          // stage s >= 1 reads the buffer written by stage s-1
-    if (s == 0 && s == last) rstage_any<T2>(R, ld, st, f.n, Ns, tw, lane);
-    else if (s == 0) rstage_any<T2>(R, ld, sA, f.n, Ns, tw, lane);
-    else if (s == last) { if (in_A) rstage_any<T2>(R, lA, st, f.n, Ns, tw, lane); else rstage_any<T2>(R, lB, st, f.n, Ns, tw, lane); }
-    else { if (in_A) rstage_any<T2>(R, lA, sB, f.n, Ns, tw, lane); else rstage_any<T2>(R, lB, sA, f.n, Ns, tw, lane); }
+    if (s == 0 && s == last) rstage_any<T2, PRIMES>(R, ld, st, f.n, Ns, tw, lane);
+    else if (s == 0) rstage_any<T2, PRIMES>(R, ld, sA, f.n, Ns, tw, lane);
+    else if (s == last) { if (in_A) rstage_any<T2, PRIMES>(R, lA, st, f.n, Ns, tw, lane); else rstage_any<T2, PRIMES>(R, lB, st, f.n, Ns, tw, lane); }
+    else { if (in_A) rstage_any<T2, PRIMES>(R, lA, sB, f.n, Ns, tw, lane); else rstage_any<T2, PRIMES>(R, lB, sA, f.n, Ns, tw, lane); }
     Ns *= R;
   }
 }

@@ -64,7 +64,7 @@ template <> struct Es<double> {
 
 // ---------------------------------------------------------------- optional stage profiler (debug builds only)
 #ifdef FBSPCA_PHASE_PROF
-__device__ unsigned long long g_phase_prof[1024 * 8];
+static __device__ unsigned long long g_phase_prof[1024 * 8];
 #define PROF_INIT() unsigned long long _pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long _pt = clock64();
 #define PROF_MARK(i) do { if (threadIdx.x == 0) { long long _n = clock64(); _pacc[i] += _n - _pt; _pt = _n; } } while (0)
 #define PROF_STORE() do { if (threadIdx.x == 0) for (int _i = 0; _i < 8; ++_i) g_phase_prof[blockIdx.x * 8 + _i] = _pacc[_i]; } while (0)
@@ -509,7 +509,8 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           };
           const int kmx = pp.k_max;
           auto st = [&](int t, T2 v) { if (t <= kmx) stg[(size_t)t * GS + jj] = v; };
-          fft_any<T2, NC>(pp.fft_theta, ld, st, angA, angB, twT, lane);
+          if constexpr (NC > 0) fft_pow2<T2, NC>(ld, st, angA, angB, twT, lane);
+          else fft_rt<T2, sizeof(T) == 4>(pp.fft_theta, ld, st, angA, angB, twT, lane);
         }
       }
       if (j0 == 0 && want_prefetch) { issue_image(img + gridDim.x); prefetched = true; }
@@ -569,21 +570,8 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
   PROF_STORE();
 }
 
-int polar_max_smem() { return 227 * 1024; }
-
-#ifdef FBSPCA_PHASE_PROF
-extern "C" int fbspca_debug_phase_prof(unsigned long long* out, int n) {
-  return (int)cudaMemcpyFromSymbol(out, g_phase_prof, sizeof(unsigned long long) * n);
-}
-#endif
-
-int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps) {
-  return (int)(((sizeof(PolarParams) + 15) / 16) * 16) + (int)((((M + n_theta) * csz + L * (csz / 2)) + 15) / 16) * 16 +
-         nwarps * 2 * ((M + 15) & ~15) * csz;
-}
-
 template <typename T, int W, int MC>
-static cudaError_t launch_polar_t(const Plan& P, const void* d_images, int64_t n_img, int64_t stride,
+cudaError_t launch_polar_t(const Plan& P, const void* d_images, int64_t n_img, int64_t stride,
                                   cudaStream_t s) {
   auto kern = polar_kernel<T, W, MC>;
   static int configured = 0;
@@ -596,6 +584,59 @@ static cudaError_t launch_polar_t(const Plan& P, const void* d_images, int64_t n
   kern<<<grid, P.pp.nwarps * 32, P.polar_smem, s>>>(P.d_pp, reinterpret_cast<const T*>(d_images), n_img, stride,
                                                     reinterpret_cast<T*>(P.d_ghat));
   return cudaGetLastError();
+}
+
+// The instantiations compile in parallel: build.py compiles this file once per part (FBSPCA_POLAR_PART = 1..5
+// via csrc/polar_part*.cu, each one heavy kernel or two) and once as the dispatcher (part 0).  Phase-profiling
+// builds (a __device__ counter array) define FBSPCA_POLAR_SINGLE_TU and instantiate everything in part 0.
+#ifndef FBSPCA_POLAR_PART
+#define FBSPCA_POLAR_PART 0
+#endif
+#ifdef FBSPCA_POLAR_SINGLE_TU
+#define FBSPCA_POLAR_HERE(part) (FBSPCA_POLAR_PART == 0)
+#else
+#define FBSPCA_POLAR_HERE(part) (FBSPCA_POLAR_PART == (part))
+#endif
+#define FBSPCA_POLAR_INST(T, W, MC) \
+  template cudaError_t launch_polar_t<T, W, MC>(const Plan&, const void*, int64_t, int64_t, cudaStream_t);
+#define FBSPCA_POLAR_EXTERN(T, W, MC) \
+  extern template cudaError_t launch_polar_t<T, W, MC>(const Plan&, const void*, int64_t, int64_t, cudaStream_t);
+#define FBSPCA_POLAR_LIST(X, P1, P2, P3, P4, P5) \
+  P1(X(float, 6, 256)) P2(X(float, 6, 512)) P2(X(float, 6, 128)) P3(X(float, 6, 0)) P4(X(float, 7, 0)) \
+  P4(X(float, 8, 0)) P5(X(double, 13, 0)) P5(X(double, 13, 64))
+#define FBSPCA_ON(x) x
+#define FBSPCA_OFF(x)
+#if FBSPCA_POLAR_HERE(1)
+FBSPCA_POLAR_LIST(FBSPCA_POLAR_INST, FBSPCA_ON, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF)
+#endif
+#if FBSPCA_POLAR_HERE(2)
+FBSPCA_POLAR_LIST(FBSPCA_POLAR_INST, FBSPCA_OFF, FBSPCA_ON, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF)
+#endif
+#if FBSPCA_POLAR_HERE(3)
+FBSPCA_POLAR_LIST(FBSPCA_POLAR_INST, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_ON, FBSPCA_OFF, FBSPCA_OFF)
+#endif
+#if FBSPCA_POLAR_HERE(4)
+FBSPCA_POLAR_LIST(FBSPCA_POLAR_INST, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_ON, FBSPCA_OFF)
+#endif
+#if FBSPCA_POLAR_HERE(5)
+FBSPCA_POLAR_LIST(FBSPCA_POLAR_INST, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_ON)
+#endif
+
+#if FBSPCA_POLAR_PART == 0
+#ifndef FBSPCA_POLAR_SINGLE_TU
+FBSPCA_POLAR_LIST(FBSPCA_POLAR_EXTERN, FBSPCA_ON, FBSPCA_ON, FBSPCA_ON, FBSPCA_ON, FBSPCA_ON)
+#endif
+int polar_max_smem() { return 227 * 1024; }
+
+#ifdef FBSPCA_PHASE_PROF
+extern "C" int fbspca_debug_phase_prof(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_phase_prof, sizeof(unsigned long long) * n);
+}
+#endif
+
+int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps) {
+  return (int)(((sizeof(PolarParams) + 15) / 16) * 16) + (int)((((M + n_theta) * csz + L * (csz / 2)) + 15) / 16) * 16 +
+         nwarps * 2 * ((M + 15) & ~15) * csz;
 }
 
 cudaError_t launch_polar(const Plan& P, const void* d_images, int64_t n_img, int64_t stride, cudaStream_t s) {
@@ -620,5 +661,7 @@ cudaError_t launch_polar(const Plan& P, const void* d_images, int64_t n_img, int
     default: return cudaErrorInvalidValue;
   }
 }
+
+#endif  // FBSPCA_POLAR_PART == 0
 
 }  // namespace fbspca

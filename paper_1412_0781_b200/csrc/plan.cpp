@@ -324,8 +324,8 @@ fbspca_status build_host_plan(Plan& P) {
   pp.S = S;
   // pow2 plans (n_theta = 2 M, M in {64..512}) run the ring FFTs as pairs of half-length FFTs in the per-warp
   // FFT scratch (kernels_polar.cu K3): the staging [k][ring] for 32 rings is all the region holds then
-  const bool pow2_kernel = M == 64 || M == 128 || M == 256 || M == 512;
-  const bool ring_pairs = P.n_theta == 2 * M && !getenv("FBSPCA_NO_RT_PAIRS") ;
+  const bool pow2_kernel = M == 64 || M == 128 || M == 256 || M == 512;   // compile-time FFT kernels (launch_polar)
+  const bool ring_pairs = P.n_theta == 2 * M && !getenv("FBSPCA_NO_RT_PAIRS");
   pp.ring_pairs = ring_pairs ? 1 : 0;
   if (ring_pairs) {
     Gsel = std::min(32, P.n_xi);
@@ -364,7 +364,7 @@ fbspca_status build_host_plan(Plan& P) {
     const int last = std::min(phase_lo[p] + S - 1, b2max + w - 1);
     return (u2 + w <= last) ? p : -1;
   };
-  const bool doubles = P.dt == FBSPCA_F32 && w == 6 && ring_pairs && pow2_kernel && !getenv("FBSPCA_NO_DOUBLES");
+  const bool doubles = P.dt == FBSPCA_F32 && w == 6 && pow2_kernel && !getenv("FBSPCA_NO_DOUBLES");
   std::vector<std::vector<std::array<int, 3>>> ph_single(phase_lo.size()), ph_double(phase_lo.size());
   std::vector<uint32_t> singles;
   std::vector<std::array<uint32_t, 2>> dbl;

@@ -20,7 +20,7 @@ def build():
     for src in B.SRC:
         obj = os.path.join("/tmp", "prof_" + os.path.basename(src) + ".o")
         subprocess.check_call([B.NVCC] + [f for f in B.FLAGS if f != "-v" and f != "-Xptxas"] +
-                              ["-DFBSPCA_PHASE_PROF", "-c", os.path.join(B.PKG, src), "-o", obj])
+                              ["-DFBSPCA_PHASE_PROF", "-DFBSPCA_POLAR_SINGLE_TU", "-c", os.path.join(B.PKG, src), "-o", obj])
         objs.append(obj)
     subprocess.check_call([B.NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", PROF_LIB] + objs + ["-ldl"])
 
