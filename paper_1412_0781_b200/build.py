@@ -7,7 +7,7 @@ import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-SRC = (["csrc/plan.cpp", "csrc/kernels_polar.cu"] + [f"csrc/polar_part{i}.cu" for i in range(1, 6)] +
+SRC = (["csrc/plan.cpp", "csrc/kernels_polar.cu"] + [f"csrc/polar_part{i}.cu" for i in range(1, 7)] +
        ["csrc/kernels_linalg.cu", "csrc/kernels_tma.cu", "csrc/kernels_synth.cu", "csrc/kernels_params.cu", "csrc/capi.cu"])
 HDR = ["csrc/internal.h", "csrc/fft_device.cuh", "csrc/kernels_polar.cu", os.path.join("..", "include", "fbspca.h")]
 LIB = os.path.join(PKG, "lib", "libfbspca.so")

@@ -114,7 +114,7 @@ __device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tws,
         if (HZ && R >= 4 && r >= R / 4 && r < 3 * R / 4) v[r] = T2{0, 0};
         else v[r] = ld(j + r * NB);
       }
-      const int jm = j & (Ns - 1);
+      const int jm = j % Ns;                      // compile-time Ns: a mask for powers of two
       if constexpr (Ns > 1) {
 #pragma unroll
         for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tws[TOFF + (r - 1) * Ns + jm]);
@@ -133,8 +133,9 @@ __device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tws,
 // (unswizzled: 2.1x).
 __device__ __forceinline__ int padi(int i) { return i ^ ((3 * (i >> 4)) & 15); }
 
-// which ping-pong buffer the last stage of fft_pow2<N> does NOT read (so the result may be stored there)
-template <int N> __host__ __device__ constexpr bool fft_result_in_A() { return N == 128 || N == 256 || N == 512; }
+// which ping-pong buffer the last stage of fft_ct<N> does NOT read (so the result may be stored there)
+// (odd stage count: 128, 256, 512 = 3 stages, 720 = 5; even: 64, 1024, 600)
+template <int N> __host__ __device__ constexpr bool fft_result_in_A() { return N == 128 || N == 256 || N == 512 || N == 720; }
 
 // stage list per size: (R, Ns) ... ; table offsets TOFF accumulate (R - 1) Ns over stages with Ns > 1
 template <typename T2, int R, int Ns>
@@ -161,14 +162,21 @@ __device__ void build_stage_tw(T2* dst, const T2* __restrict__ lin, int tid, int
   } else if constexpr (N == 1024) {
     fill_stage_tw<T2, 8, 8>(dst, lin, N, tid, nthr); fill_stage_tw<T2, 4, 64>(dst + 56, lin, N, tid, nthr);
     fill_stage_tw<T2, 4, 256>(dst + 248, lin, N, tid, nthr);
+  } else if constexpr (N == 600) {
+    fill_stage_tw<T2, 5, 8>(dst, lin, N, tid, nthr); fill_stage_tw<T2, 5, 40>(dst + 32, lin, N, tid, nthr);
+    fill_stage_tw<T2, 3, 200>(dst + 192, lin, N, tid, nthr);
+  } else if constexpr (N == 720) {
+    fill_stage_tw<T2, 5, 8>(dst, lin, N, tid, nthr); fill_stage_tw<T2, 3, 40>(dst + 32, lin, N, tid, nthr);
+    fill_stage_tw<T2, 3, 120>(dst + 112, lin, N, tid, nthr); fill_stage_tw<T2, 2, 360>(dst + 352, lin, N, tid, nthr);
   } else {
     for (int i = tid; i < N; i += nthr) dst[i] = lin[i];     // runtime path: linear table
   }
 }
 
-// Compile-time power-of-two FFT: first stage reads ld(), last stage writes st(), ping-pong in A, B.
+// Compile-time FFT (powers of two 64..1024, and 600 / 720): first stage reads ld(), last stage writes st(),
+// ping-pong in A, B.
 template <typename T2, int N, bool HZ = false, class Ld, class St>
-__device__ __forceinline__ void fft_pow2(Ld ld, St st, T2* A, T2* B, const T2* tw, int lane) {
+__device__ __forceinline__ void fft_ct(Ld ld, St st, T2* A, T2* B, const T2* tw, int lane) {
   auto lA = [A](int i) { return A[padi(i)]; };
   auto lB = [B](int i) { return B[padi(i)]; };
   auto sA = [A](int i, T2 v) { A[padi(i)] = v; };
@@ -187,6 +195,13 @@ __device__ __forceinline__ void fft_pow2(Ld ld, St st, T2* A, T2* B, const T2* t
   } else if constexpr (N == 1024) {
     cstage<T2, 1024, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 1024, 8, 8, 0>(lA, sB, tw, lane);
     cstage<T2, 1024, 4, 64, 56>(lB, sA, tw, lane); cstage<T2, 1024, 4, 256, 248>(lA, st, tw, lane);
+  } else if constexpr (N == 600) {          // 8 5 5 3 (the paper's Table III images, L = 300)
+    cstage<T2, 600, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 600, 5, 8, 0>(lA, sB, tw, lane);
+    cstage<T2, 600, 5, 40, 32>(lB, sA, tw, lane); cstage<T2, 600, 3, 200, 192>(lA, st, tw, lane);
+  } else if constexpr (N == 720) {          // 8 5 3 3 2 (C5, L = 360)
+    cstage<T2, 720, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 720, 5, 8, 0>(lA, sB, tw, lane);
+    cstage<T2, 720, 3, 40, 32>(lB, sA, tw, lane); cstage<T2, 720, 3, 120, 112>(lA, sB, tw, lane);
+    cstage<T2, 720, 2, 360, 352>(lB, st, tw, lane);
   } else {
     static_assert(N == 64, "unsupported compile-time FFT size");
   }
@@ -285,7 +300,7 @@ __device__ void fft_rt(const FftPlan& f, Ld ld, St st, T2* A, T2* B, const T2* t
 
 template <typename T2, int NC, bool HZ = false, class Ld, class St>
 __device__ __forceinline__ void fft_any(const FftPlan& f, Ld ld, St st, T2* A, T2* B, const T2* tw, int lane) {
-  if constexpr (NC > 0) fft_pow2<T2, NC, HZ>(ld, st, A, B, tw, lane);
+  if constexpr (NC > 0) fft_ct<T2, NC, HZ>(ld, st, A, B, tw, lane);
   else fft_rt<T2>(f, ld, st, A, B, tw, lane);
 }
 

@@ -393,11 +393,11 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           load_pair(j0 + G);                          // next group's inputs, consumed one iteration later
           // stage-1 index t = lane + 32 r  ->  r = (t - lane) >> 5 (compile-time after unrolling)
           auto ldu = [&](int t) -> T2 { const int r = (t - lane) >> 5; return T2{ca[r].x, cb[r].x}; };
-          fft_pow2<T2, MC>(ldu, stR, myA, myB, twM, lane);
+          fft_ct<T2, MC>(ldu, stR, myA, myB, twM, lane);
           __syncwarp();
           for (int m = lane; 2 * m <= kmx; m += 32) {
             const T2 u = res[padi(m)];
-            T2 uc = res[padi((MC - m) & (MC - 1))];
+            T2 uc = res[padi(m == 0 ? 0 : MC - m)];
             uc.y = -uc.y;
             const T2 sp = cadd(u, uc), dm = csub(u, uc);
             stg[(size_t)(2 * m) * GS + jj] = sp;
@@ -409,7 +409,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             const int r = (t - lane) >> 5;
             return cmul(T2{ca[r].y, cb[r].y}, twT[t]);
           };
-          fft_pow2<T2, MC>(ldv, stR, myA, myB, twM, lane);
+          fft_ct<T2, MC>(ldv, stR, myA, myB, twM, lane);
           __syncwarp();
           for (int m = lane; 2 * m + 1 <= kmx; m += 32) {
             const T2 v = res[padi(m)];
@@ -434,11 +434,11 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           const T2* fa = Pol + (int64_t)(j0 + jj) * half;
           const T2* fb = two ? fa + half : fa;
           auto ldu = [&](int t) -> T2 { const T2 a = fa[t], b = fb[t]; return T2{a.x, two ? b.x : T(0)}; };
-          fft_pow2<T2, MC>(ldu, stR, myA, myB, twM, lane);
+          fft_ct<T2, MC>(ldu, stR, myA, myB, twM, lane);
           __syncwarp();
           for (int m = lane; 2 * m <= kmx; m += 32) {
             const T2 u = res[padi(m)];
-            T2 uc = res[padi((MC - m) & (MC - 1))];
+            T2 uc = res[padi(m == 0 ? 0 : MC - m)];
             uc.y = -uc.y;
             const T2 sp = cadd(u, uc), dm = csub(u, uc);
             stg[(size_t)(2 * m) * GS + jj] = sp;
@@ -449,7 +449,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             const T2 a = fa[t], b = fb[t];
             return cmul(T2{a.y, two ? b.y : T(0)}, twT[t]);
           };
-          fft_pow2<T2, MC>(ldv, stR, myA, myB, twM, lane);
+          fft_ct<T2, MC>(ldv, stR, myA, myB, twM, lane);
           __syncwarp();
           for (int m = lane; 2 * m + 1 <= kmx; m += 32) {
             const T2 v = res[padi(m)];
@@ -509,7 +509,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           };
           const int kmx = pp.k_max;
           auto st = [&](int t, T2 v) { if (t <= kmx) stg[(size_t)t * GS + jj] = v; };
-          if constexpr (NC > 0) fft_pow2<T2, NC>(ld, st, angA, angB, twT, lane);
+          if constexpr (NC > 0) fft_ct<T2, NC>(ld, st, angA, angB, twT, lane);
           else fft_rt<T2, sizeof(T) == 4>(pp.fft_theta, ld, st, angA, angB, twT, lane);
         }
       }
@@ -586,7 +586,7 @@ cudaError_t launch_polar_t(const Plan& P, const void* d_images, int64_t n_img, i
   return cudaGetLastError();
 }
 
-// The instantiations compile in parallel: build.py compiles this file once per part (FBSPCA_POLAR_PART = 1..5
+// The instantiations compile in parallel: build.py compiles this file once per part (FBSPCA_POLAR_PART = 1..6
 // via csrc/polar_part*.cu, each one heavy kernel or two) and once as the dispatcher (part 0).  Phase-profiling
 // builds (a __device__ counter array) define FBSPCA_POLAR_SINGLE_TU and instantiate everything in part 0.
 #ifndef FBSPCA_POLAR_PART
@@ -601,30 +601,34 @@ cudaError_t launch_polar_t(const Plan& P, const void* d_images, int64_t n_img, i
   template cudaError_t launch_polar_t<T, W, MC>(const Plan&, const void*, int64_t, int64_t, cudaStream_t);
 #define FBSPCA_POLAR_EXTERN(T, W, MC) \
   extern template cudaError_t launch_polar_t<T, W, MC>(const Plan&, const void*, int64_t, int64_t, cudaStream_t);
-#define FBSPCA_POLAR_LIST(X, P1, P2, P3, P4, P5) \
+#define FBSPCA_POLAR_LIST(X, P1, P2, P3, P4, P5, P6) \
   P1(X(float, 6, 256)) P2(X(float, 6, 512)) P2(X(float, 6, 128)) P3(X(float, 6, 0)) P4(X(float, 7, 0)) \
-  P4(X(float, 8, 0)) P5(X(double, 13, 0)) P5(X(double, 13, 64))
+  P4(X(float, 8, 0)) P5(X(double, 13, 0)) P5(X(double, 13, 64)) P6(X(float, 6, 600)) P6(X(float, 6, 720))
 #define FBSPCA_ON(x) x
 #define FBSPCA_OFF(x)
 #if FBSPCA_POLAR_HERE(1)
-FBSPCA_POLAR_LIST(FBSPCA_POLAR_INST, FBSPCA_ON, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF)
+FBSPCA_POLAR_LIST(FBSPCA_POLAR_INST, FBSPCA_ON, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF)
 #endif
 #if FBSPCA_POLAR_HERE(2)
-FBSPCA_POLAR_LIST(FBSPCA_POLAR_INST, FBSPCA_OFF, FBSPCA_ON, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF)
+FBSPCA_POLAR_LIST(FBSPCA_POLAR_INST, FBSPCA_OFF, FBSPCA_ON, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF)
 #endif
 #if FBSPCA_POLAR_HERE(3)
-FBSPCA_POLAR_LIST(FBSPCA_POLAR_INST, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_ON, FBSPCA_OFF, FBSPCA_OFF)
+FBSPCA_POLAR_LIST(FBSPCA_POLAR_INST, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_ON, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF)
 #endif
 #if FBSPCA_POLAR_HERE(4)
-FBSPCA_POLAR_LIST(FBSPCA_POLAR_INST, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_ON, FBSPCA_OFF)
+FBSPCA_POLAR_LIST(FBSPCA_POLAR_INST, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_ON, FBSPCA_OFF, FBSPCA_OFF)
 #endif
 #if FBSPCA_POLAR_HERE(5)
-FBSPCA_POLAR_LIST(FBSPCA_POLAR_INST, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_ON)
+FBSPCA_POLAR_LIST(FBSPCA_POLAR_INST, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_ON, FBSPCA_OFF)
+#endif
+
+#if FBSPCA_POLAR_HERE(6)
+FBSPCA_POLAR_LIST(FBSPCA_POLAR_INST, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_OFF, FBSPCA_ON)
 #endif
 
 #if FBSPCA_POLAR_PART == 0
 #ifndef FBSPCA_POLAR_SINGLE_TU
-FBSPCA_POLAR_LIST(FBSPCA_POLAR_EXTERN, FBSPCA_ON, FBSPCA_ON, FBSPCA_ON, FBSPCA_ON, FBSPCA_ON)
+FBSPCA_POLAR_LIST(FBSPCA_POLAR_EXTERN, FBSPCA_ON, FBSPCA_ON, FBSPCA_ON, FBSPCA_ON, FBSPCA_ON, FBSPCA_ON)
 #endif
 int polar_max_smem() { return 227 * 1024; }
 
@@ -640,7 +644,8 @@ int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps) {
 }
 
 cudaError_t launch_polar(const Plan& P, const void* d_images, int64_t n_img, int64_t stride, cudaStream_t s) {
-  const bool pow2 = P.n_theta == 2 * P.M && (P.M == 64 || P.M == 128 || P.M == 256 || P.M == 512);
+  const bool pow2 = P.n_theta == 2 * P.M && (P.M == 64 || P.M == 128 || P.M == 256 || P.M == 512 || P.M == 600 ||
+                                              P.M == 720);      // compile-time FFT kernels
   if (P.dt == FBSPCA_F64) {
     if (P.w != 13) return cudaErrorInvalidValue;
     if (pow2 && P.M == 64) return launch_polar_t<double, 13, 64>(P, d_images, n_img, stride, s);
@@ -651,6 +656,8 @@ cudaError_t launch_polar(const Plan& P, const void* d_images, int64_t n_img, int
       case 128: return launch_polar_t<float, 6, 128>(P, d_images, n_img, stride, s);
       case 256: return launch_polar_t<float, 6, 256>(P, d_images, n_img, stride, s);
       case 512: return launch_polar_t<float, 6, 512>(P, d_images, n_img, stride, s);
+      case 600: return launch_polar_t<float, 6, 600>(P, d_images, n_img, stride, s);
+      case 720: return launch_polar_t<float, 6, 720>(P, d_images, n_img, stride, s);
       default: break;
     }
   }

@@ -324,7 +324,7 @@ fbspca_status build_host_plan(Plan& P) {
   pp.S = S;
   // pow2 plans (n_theta = 2 M, M in {64..512}) run the ring FFTs as pairs of half-length FFTs in the per-warp
   // FFT scratch (kernels_polar.cu K3): the staging [k][ring] for 32 rings is all the region holds then
-  const bool pow2_kernel = M == 64 || M == 128 || M == 256 || M == 512;   // compile-time FFT kernels (launch_polar)
+  const bool pow2_kernel = M == 64 || M == 128 || M == 256 || M == 512 || M == 600 || M == 720;   // compile-time FFT kernels (launch_polar)
   const bool ring_pairs = P.n_theta == 2 * M && !getenv("FBSPCA_NO_RT_PAIRS");
   pp.ring_pairs = ring_pairs ? 1 : 0;
   if (ring_pairs) {
