@@ -115,6 +115,14 @@ def work_per_image(plan, L):
                 algorithmic_bytes=b_img + b_coef)
 
 
+# Workloads beyond BASELINE.json's configs, and the paper's own number for the same workload (BASELINE.md §1:
+# images/s = n / (expansion + steerable PCA time), 60-core CPU machine -- context, another machine).
+WORKLOADS = {"T3": "T3: the paper's Table III workload (P:481-501)",
+             "RB": "RB: the paper's ribosome experiment shape (P:518, P:536; synthetic blobs, dataset absent)"}
+PAPER_IMG_S = {"T3": (1e5 / (1438.0 + 42.0), "P:490-492: 1,438 s expansion + 42 s steerable PCA, n = 10^5"),
+               "RB": (1e5 / (9 * 60.0 + 12.0), "P:565: 9 min FB coefficients + 12 s sPCA, n = 10^5")}
+
+
 def cpu_baseline(cfg, seconds_target=15.0):
     """The oracle as it stands (expansion + covariance) on a bounded sample of the same workload."""
     import numpy as np
@@ -343,10 +351,10 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32" if dt == F.F32 else "f64", "data": "synthetic",
+            "vs_baseline": (value / PAPER_IMG_S[cfg["name"]][0]) if cfg["name"] in PAPER_IMG_S else None,
+            "dtype": "f32" if dt == F.F32 else "f64", "data": "synthetic",
             "config": {"workload": (f"{cfg['name']}: BASELINE.json configs[{int(cfg['name'][1]) - 1}]"
-                                    if cfg["name"].startswith("C") else
-                                    f"{cfg['name']}: the paper's Table III workload (P:481-501)"), "n": n,
+                                    if cfg["name"].startswith("C") else WORKLOADS[cfg["name"]]), "n": n,
                        "L": cfg["L"], "R": cfg["R"], "c": cfg["c"], "parallelism": f"dp{world}",
                        "n_per_rank": n_local, "eps": 1e-5, "M": plan.M, "w": plan.w,
                        "l2": f"inputs larger than L2 ({n * cfg['L'] * cfg['L'] * (4 if dt == F.F32 else 8) / 1e9:.1f} GB "
@@ -368,6 +376,8 @@ def main():
         }
         if e2e:
             line["e2e"] = e2e
+        if cfg["name"] in PAPER_IMG_S:
+            line["vs_baseline_source"] = PAPER_IMG_S[cfg["name"]][1] + " (60 CPU cores, another machine: context)"
         if world == 1 and not args.no_cpu_baseline:
             try:
                 line["cpu_baseline"] = cpu_baseline(cfg)
