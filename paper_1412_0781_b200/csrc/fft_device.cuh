@@ -101,13 +101,20 @@ template <typename T2> struct Dft<T2, 5> {
 // conflicts), built once per CTA by build_stage_tw<N>.
 // HZ (first stage only): inputs t in [N/4, 3N/4) are known zeros -- the zero-padded rows / columns of K1
 // (pixel index L/2 <= M/4 away from 0 on both sides) -- so those butterfly legs are constant zeros.
-template <typename T2, int N, int R, int Ns, int TOFF, class Ld, class St, bool HZ = false>
-__device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tws, int lane) {
+// GS: lanes per FFT (32 = one warp; 64 = a warp pair synchronised on named barrier `bar`, for sizes whose two
+// ping-pong buffers per warp do not fit 16 warps -- the pair shares one buffer set, so all 16 warps work).
+template <int GS> __device__ __forceinline__ void gsync(int bar) {
+  if constexpr (GS == 32) __syncwarp();
+  else asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(GS) : "memory");
+}
+
+template <typename T2, int N, int R, int Ns, int TOFF, bool HZ = false, int GS = 32, class Ld, class St>
+__device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tws, int lane, int bar = 0) {
   constexpr int NB = N / R;
 #pragma unroll
-  for (int j0 = 0; j0 < NB; j0 += 32) {
+  for (int j0 = 0; j0 < NB; j0 += GS) {
     const int j = j0 + lane;
-    if (NB % 32 == 0 || j < NB) {
+    if (NB % GS == 0 || j < NB) {
       T2 v[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -125,7 +132,7 @@ __device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tws,
       for (int r = 0; r < R; ++r) st(idxD + r * Ns, v[r]);
     }
   }
-  __syncwarp();
+  gsync<GS>(bar);
 }
 
 // Ping-pong scratch index swizzle: XOR the low 4 bits with 3 (i >> 4).  64-bit shared accesses resolve per
@@ -175,33 +182,35 @@ __device__ void build_stage_tw(T2* dst, const T2* __restrict__ lin, int tid, int
 
 // Compile-time FFT (powers of two 64..1024, and 600 / 720): first stage reads ld(), last stage writes st(),
 // ping-pong in A, B.
-template <typename T2, int N, bool HZ = false, class Ld, class St>
-__device__ __forceinline__ void fft_ct(Ld ld, St st, T2* A, T2* B, const T2* tw, int lane) {
+template <typename T2, int N, bool HZ = false, int GS = 32, class Ld, class St>
+__device__ __forceinline__ void fft_ct(Ld ld, St st, T2* A, T2* B, const T2* tw, int lane, int bar = 0) {
   auto lA = [A](int i) { return A[padi(i)]; };
   auto lB = [B](int i) { return B[padi(i)]; };
   auto sA = [A](int i, T2 v) { A[padi(i)] = v; };
   auto sB = [B](int i, T2 v) { B[padi(i)] = v; };
   if constexpr (N == 64) {
-    cstage<T2, 64, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 64, 8, 8, 0>(lA, st, tw, lane);
+    cstage<T2, 64, 8, 1, 0, HZ>(ld, sA, tw, lane); cstage<T2, 64, 8, 8, 0>(lA, st, tw, lane);
   } else if constexpr (N == 128) {
-    cstage<T2, 128, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 128, 4, 8, 0>(lA, sB, tw, lane);
+    cstage<T2, 128, 8, 1, 0, HZ>(ld, sA, tw, lane); cstage<T2, 128, 4, 8, 0>(lA, sB, tw, lane);
     cstage<T2, 128, 4, 32, 24>(lB, st, tw, lane);
   } else if constexpr (N == 256) {
-    cstage<T2, 256, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 256, 8, 8, 0>(lA, sB, tw, lane);
+    cstage<T2, 256, 8, 1, 0, HZ>(ld, sA, tw, lane); cstage<T2, 256, 8, 8, 0>(lA, sB, tw, lane);
     cstage<T2, 256, 4, 64, 56>(lB, st, tw, lane);
   } else if constexpr (N == 512) {
-    cstage<T2, 512, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 512, 8, 8, 0>(lA, sB, tw, lane);
+    cstage<T2, 512, 8, 1, 0, HZ>(ld, sA, tw, lane); cstage<T2, 512, 8, 8, 0>(lA, sB, tw, lane);
     cstage<T2, 512, 8, 64, 56>(lB, st, tw, lane);
   } else if constexpr (N == 1024) {
-    cstage<T2, 1024, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 1024, 8, 8, 0>(lA, sB, tw, lane);
+    cstage<T2, 1024, 8, 1, 0, HZ>(ld, sA, tw, lane); cstage<T2, 1024, 8, 8, 0>(lA, sB, tw, lane);
     cstage<T2, 1024, 4, 64, 56>(lB, sA, tw, lane); cstage<T2, 1024, 4, 256, 248>(lA, st, tw, lane);
   } else if constexpr (N == 600) {          // 8 5 5 3 (the paper's Table III images, L = 300)
-    cstage<T2, 600, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 600, 5, 8, 0>(lA, sB, tw, lane);
-    cstage<T2, 600, 5, 40, 32>(lB, sA, tw, lane); cstage<T2, 600, 3, 200, 192>(lA, st, tw, lane);
+    cstage<T2, 600, 8, 1, 0, HZ, GS>(ld, sA, tw, lane, bar); cstage<T2, 600, 5, 8, 0, false, GS>(lA, sB, tw, lane, bar);
+    cstage<T2, 600, 5, 40, 32, false, GS>(lB, sA, tw, lane, bar);
+    cstage<T2, 600, 3, 200, 192, false, GS>(lA, st, tw, lane, bar);
   } else if constexpr (N == 720) {          // 8 5 3 3 2 (C5, L = 360)
-    cstage<T2, 720, 8, 1, 0, decltype(ld), decltype(sA), HZ>(ld, sA, tw, lane); cstage<T2, 720, 5, 8, 0>(lA, sB, tw, lane);
-    cstage<T2, 720, 3, 40, 32>(lB, sA, tw, lane); cstage<T2, 720, 3, 120, 112>(lA, sB, tw, lane);
-    cstage<T2, 720, 2, 360, 352>(lB, st, tw, lane);
+    cstage<T2, 720, 8, 1, 0, HZ, GS>(ld, sA, tw, lane, bar); cstage<T2, 720, 5, 8, 0, false, GS>(lA, sB, tw, lane, bar);
+    cstage<T2, 720, 3, 40, 32, false, GS>(lB, sA, tw, lane, bar);
+    cstage<T2, 720, 3, 120, 112, false, GS>(lA, sB, tw, lane, bar);
+    cstage<T2, 720, 2, 360, 352, false, GS>(lB, st, tw, lane, bar);
   } else {
     static_assert(N == 64, "unsupported compile-time FFT size");
   }
@@ -298,9 +307,10 @@ __device__ void fft_rt(const FftPlan& f, Ld ld, St st, T2* A, T2* B, const T2* t
   }
 }
 
-template <typename T2, int NC, bool HZ = false, class Ld, class St>
-__device__ __forceinline__ void fft_any(const FftPlan& f, Ld ld, St st, T2* A, T2* B, const T2* tw, int lane) {
-  if constexpr (NC > 0) fft_ct<T2, NC, HZ>(ld, st, A, B, tw, lane);
+template <typename T2, int NC, bool HZ = false, int GS = 32, class Ld, class St>
+__device__ __forceinline__ void fft_any(const FftPlan& f, Ld ld, St st, T2* A, T2* B, const T2* tw, int lane,
+                                        int bar = 0) {
+  if constexpr (NC > 0) fft_ct<T2, NC, HZ, GS>(ld, st, A, B, tw, lane, bar);
   else fft_rt<T2>(f, ld, st, A, B, tw, lane);
 }
 

@@ -100,7 +100,11 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
   T2* wscr = reinterpret_cast<T2*>(base + (((size_t)(M + nt) * sizeof(T2) + (size_t)L * sizeof(T) + 15) / 16) * 16);
   const int MP = (M + 15) & ~15, NTP = (nt + 15) & ~15;   // ping-pong lengths: padi permutes within 16-blocks
   T2* region = wscr + (size_t)pp.fft_warps * 2 * MP;
-  T2* myA = wscr + (size_t)warp * 2 * MP;         // row / column FFT ping-pong
+  // FFT groups: one warp (FG = 32) or, for M = 600 / 720 (8 ping-pong pairs fit, not 16), a warp pair (FG = 64)
+  // on named barrier 1 + grp, so all 16 warps run the row / column / ring FFTs
+  constexpr int FG = (MC == 600 || MC == 720) ? 64 : 32;
+  const int grp = warp / (FG / 32), glane = tid & (FG - 1), gbar = 1 + grp;
+  T2* myA = wscr + (size_t)grp * 2 * MP;          // row / column FFT ping-pong
   T2* myB = myA + MP;
   T2* angA = region + (size_t)warp * 2 * NTP;     // angular FFT ping-pong (region is free then)
   T2* angB = angA + NTP;
@@ -153,8 +157,8 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       Isrc = simg;
     }
     // ---------------- K1a: row FFTs, two real rows per complex sequence, deapodised + zero-padded on load
-    if (warp < pp.fft_warps) {
-      for (int pr = warp; pr < (L + 1) / 2; pr += pp.fft_warps) {
+    if (grp < pp.fft_warps) {
+      for (int pr = grp; pr < (L + 1) / 2; pr += pp.fft_warps) {
         const int a0 = 2 * pr, a1 = a0 + 1;
         const bool has1 = a1 < L;
         const T* r0 = Isrc + (int64_t)a0 * L;
@@ -171,10 +175,10 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         // runtime sizes: the result goes to a per-warp slice of the (still free) phase region.
         T2* res = (MC > 0) ? (fft_result_in_A<MC>() ? myA : myB) : region + (size_t)warp * M;
         auto st = [res](int i, T2 v) { res[MC > 0 ? padi(i) : i] = v; };
-        fft_any<T2, MC, true>(pp.fft_M, ld, st, myA, myB, twM, lane);
+        fft_any<T2, MC, true, FG>(pp.fft_M, ld, st, myA, myB, twM, glane, gbar);
         const int lo0 = pp.phase_lo[0], hi0 = lo0 + (S < col_lo + ncx - lo0 ? S : col_lo + ncx - lo0);
         const int lo1 = pp.n_phase > 1 ? pp.phase_lo[1] : (1 << 30);
-        for (int cc = lane; cc < ncx; cc += 32) {
+        for (int cc = glane; cc < ncx; cc += FG) {
           int m = (col_lo + cc) % M; if (m < 0) m += M;
           int mm = M - m; if (mm == M) mm = 0;
           T2 zm = res[MC > 0 ? padi(m) : m], zc = res[MC > 0 ? padi(mm) : mm];
@@ -192,7 +196,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             if (has1) region[(size_t)a1 * S + (m2 - lo0)] = xb;
           }
         }
-        __syncwarp();
+        gsync<FG>(gbar);
       }
     }
     __syncthreads();
@@ -218,8 +222,8 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         if (ph == pp.n_phase - 1) l2_discard(X, (size_t)L * ncx * sizeof(T2), tid, nthr);
       }
       PROF_MARK(1);
-      if (warp < pp.fft_warps) {
-        for (int cc = warp; cc < ncols; cc += pp.fft_warps) {
+      if (grp < pp.fft_warps) {
+        for (int cc = grp; cc < ncols; cc += pp.fft_warps) {
           T2* col = Gc + cc;
           auto ld = [&](int t) -> T2 {
             const int a = (t < M / 2 ? t : t - M) + L / 2;
@@ -231,7 +235,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             if (m1 < -M / 2 + PADR) col[(size_t)(m1 + M + row0) * S] = v;
             if (m1 >= M / 2 - PADR) col[(size_t)(m1 - M + row0) * S] = v;
           };
-          fft_any<T2, MC, true>(pp.fft_M, ld, st, myA, myB, twM, lane);
+          fft_any<T2, MC, true, FG>(pp.fft_M, ld, st, myA, myB, twM, glane, gbar);
         }
       }
       __syncthreads();
@@ -428,15 +432,15 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         const int kmx = pp.k_max;
         T2* res = fft_result_in_A<MC>() ? myA : myB;
         auto stR = [res](int i, T2 v) { res[padi(i)] = v; };
-        for (int pr = warp; warp < pp.fft_warps && 2 * pr < g; pr += pp.fft_warps) {
+        for (int pr = grp; grp < pp.fft_warps && 2 * pr < g; pr += pp.fft_warps) {
           const int jj = 2 * pr;
           const bool two = jj + 1 < g;
           const T2* fa = Pol + (int64_t)(j0 + jj) * half;
           const T2* fb = two ? fa + half : fa;
           auto ldu = [&](int t) -> T2 { const T2 a = fa[t], b = fb[t]; return T2{a.x, two ? b.x : T(0)}; };
-          fft_ct<T2, MC>(ldu, stR, myA, myB, twM, lane);
-          __syncwarp();
-          for (int m = lane; 2 * m <= kmx; m += 32) {
+          fft_ct<T2, MC, false, FG>(ldu, stR, myA, myB, twM, glane, gbar);
+          gsync<FG>(gbar);
+          for (int m = glane; 2 * m <= kmx; m += FG) {
             const T2 u = res[padi(m)];
             T2 uc = res[padi(m == 0 ? 0 : MC - m)];
             uc.y = -uc.y;
@@ -444,14 +448,14 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             stg[(size_t)(2 * m) * GS + jj] = sp;
             if (two) stg[(size_t)(2 * m) * GS + jj + 1] = T2{dm.y, -dm.x};
           }
-          __syncwarp();
+          gsync<FG>(gbar);
           auto ldv = [&](int t) -> T2 {
             const T2 a = fa[t], b = fb[t];
             return cmul(T2{a.y, two ? b.y : T(0)}, twT[t]);
           };
-          fft_ct<T2, MC>(ldv, stR, myA, myB, twM, lane);
-          __syncwarp();
-          for (int m = lane; 2 * m + 1 <= kmx; m += 32) {
+          fft_ct<T2, MC, false, FG>(ldv, stR, myA, myB, twM, glane, gbar);
+          gsync<FG>(gbar);
+          for (int m = glane; 2 * m + 1 <= kmx; m += FG) {
             const T2 v = res[padi(m)];
             T2 vc = res[padi(MC - 1 - m)];
             vc.y = -vc.y;
@@ -459,7 +463,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             stg[(size_t)(2 * m + 1) * GS + jj] = T2{-sp.y, sp.x};
             if (two) stg[(size_t)(2 * m + 1) * GS + jj + 1] = dm;
           }
-          __syncwarp();
+          gsync<FG>(gbar);
         }
       } else if (pp.ring_pairs) {
         // runtime sizes with n_theta = 2 M: the same ring-pair scheme as above on M-point mixed-radix FFTs
