@@ -197,8 +197,8 @@ __device__ __forceinline__ void fft_ct(Ld ld, St st, T2* A, T2* B, const T2* tw,
     cstage<T2, 256, 8, 1, 0, HZ>(ld, sA, tw, lane); cstage<T2, 256, 8, 8, 0>(lA, sB, tw, lane);
     cstage<T2, 256, 4, 64, 56>(lB, st, tw, lane);
   } else if constexpr (N == 512) {
-    cstage<T2, 512, 8, 1, 0, HZ>(ld, sA, tw, lane); cstage<T2, 512, 8, 8, 0>(lA, sB, tw, lane);
-    cstage<T2, 512, 8, 64, 56>(lB, st, tw, lane);
+    cstage<T2, 512, 8, 1, 0, HZ, GS>(ld, sA, tw, lane, bar); cstage<T2, 512, 8, 8, 0, false, GS>(lA, sB, tw, lane, bar);
+    cstage<T2, 512, 8, 64, 56, false, GS>(lB, st, tw, lane, bar);
   } else if constexpr (N == 1024) {
     cstage<T2, 1024, 8, 1, 0, HZ>(ld, sA, tw, lane); cstage<T2, 1024, 8, 8, 0>(lA, sB, tw, lane);
     cstage<T2, 1024, 4, 64, 56>(lB, sA, tw, lane); cstage<T2, 1024, 4, 256, 248>(lA, st, tw, lane);

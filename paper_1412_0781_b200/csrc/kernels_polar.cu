@@ -100,9 +100,9 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
   T2* wscr = reinterpret_cast<T2*>(base + (((size_t)(M + nt) * sizeof(T2) + (size_t)L * sizeof(T) + 15) / 16) * 16);
   const int MP = (M + 15) & ~15, NTP = (nt + 15) & ~15;   // ping-pong lengths: padi permutes within 16-blocks
   T2* region = wscr + (size_t)pp.fft_warps * 2 * MP;
-  // FFT groups: one warp (FG = 32) or, for M = 600 / 720 (8 ping-pong pairs fit, not 16), a warp pair (FG = 64)
+  // FFT groups: one warp (FG = 32) or, for M = 512 / 600 / 720 (8 ping-pong pairs fit, not 16), a warp pair (FG = 64)
   // on named barrier 1 + grp, so all 16 warps run the row / column / ring FFTs
-  constexpr int FG = (MC == 600 || MC == 720) ? 64 : 32;
+  constexpr int FG = (MC == 512 || MC == 600 || MC == 720) ? 64 : 32;
   const int grp = warp / (FG / 32), glane = tid & (FG - 1), gbar = 1 + grp;
   T2* myA = wscr + (size_t)grp * 2 * MP;          // row / column FFT ping-pong
   T2* myB = myA + MP;
