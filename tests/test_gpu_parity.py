@@ -302,6 +302,25 @@ def test_c3_full_size_spectral_parity():
     _spectral_checks(plan, blocks, mean, evals, evecs, m_o, C_o)
 
 
+def test_c5_full_size_sampled_expansion():
+    """configs[4] at full size (50,000 images of 360 x 360) in bench.py's launch configuration (25,000-image
+    expand batches): the last image of each batch (the CTAs' ragged tail) against the fp64 oracle."""
+    cfg = synth.config("C5")
+    n = cfg["n"]
+    imgs = synth.blob_images(cfg, 0, n, device=DEV)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=25000)
+    coeffs = F.fbspca_expand(plan, imgs)
+    torch.cuda.synchronize()
+    pick = [24999, n - 1]
+    sample = imgs[pick].double().cpu().numpy()
+    got = coeffs[:, pick].cpu().numpy().astype(np.complex128)
+    del imgs, coeffs
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    ref = O.to_flat(O.expand(sample, basis, chunk=1))
+    rel = rel_l2_per_image(got, ref, basis)
+    assert rel.max() <= TOL32, f"max per-image rel l2 {rel.max():.3e}"
+
+
 @pytest.mark.parametrize("name,n", [("C4", 2048), ("C5", 1024), ("RB", 2048)])
 def test_large_L_spectral_parity_subset(name, n):
     """configs[3] (L = 256, pow2 kernels, R = 128 tensor-core covariance) and configs[4] (L = 360, runtime
