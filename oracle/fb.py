@@ -139,36 +139,41 @@ def radial_table(basis: Basis, xi=None, w=None):
 # --------------------------------------------------------------------------
 # O5 direct Fourier sum at the polar nodes (Eq. (nufft); Q1 unit prefactor)
 # --------------------------------------------------------------------------
-def polar_ft_direct(images: np.ndarray, basis: Basis, chunk: int = 4) -> np.ndarray:
-    """F(I)(xi_1, xi_2) = sum_{i1,i2} I(i1,i2) exp(-2 pi i (xi_1 i1 + xi_2 i2)).
+def polar_ft_direct(images: np.ndarray, basis: Basis, chunk: int | None = None,
+                    node_chunk: int = 1024) -> np.ndarray:
+    """F(I)(xi_1, xi_2) = sum_{i1,i2} I(i1,i2) exp(-2 pi i (xi_1 i1 + xi_2 i2))   (Eq. (nufft), Q1 unit prefactor).
 
-    Evaluated exactly (up to rounding) at every node (xi_j cos theta_l, xi_j sin theta_l),
-    l = 0..n_theta-1.  Nodes l < n_theta/2 are summed directly; for even n_theta the node
-    l + n_theta/2 is the negated node l, where the sum for a real image is the complex
-    conjugate (exact identity of the definition for real I).
+    Evaluated exactly (up to rounding) at every node (xi_j cos theta_l, xi_j sin theta_l) as one matrix
+    product F = I_flat K^T with the dense kernel K[node, (i1, i2)] = e^{-2 pi i xi_1 i1} e^{-2 pi i xi_2 i2}
+    (built per block of node_chunk nodes; fp64 BLAS through torch).  Nodes l < n_theta/2 are summed directly;
+    for even n_theta the node l + n_theta/2 is the negated node l, where the sum for a real image is the
+    complex conjugate (exact identity of the definition for real I).  `chunk` is accepted for
+    compatibility and ignored (all images go through each kernel block at once).
     Returns (n, n_xi, n_theta) complex128.
     """
+    import torch
     images = np.asarray(images, dtype=np.float64)
     n, L, L2 = images.shape
     assert L == L2
     xi, _, theta = polar_grid(basis)
     nt = basis.n_theta
     half = nt // 2 if nt % 2 == 0 else nt
-    idx = np.arange(L) - L // 2                                   # i = a - floor(L/2)
-    k1 = np.outer(xi, np.cos(theta[:half])).ravel()               # xi_1 at nodes
-    k2 = np.outer(xi, np.sin(theta[:half])).ravel()               # xi_2 at nodes
-    E1 = np.exp(-2j * np.pi * np.outer(k1, idx))                  # (nodes, L): e^{-2pi i xi1 i1}
-    E2 = np.exp(-2j * np.pi * np.outer(k2, idx))                  # (nodes, L): e^{-2pi i xi2 i2}
+    idx = torch.arange(L, dtype=torch.float64) - L // 2                       # i = a - floor(L/2)
+    k1 = torch.from_numpy(np.outer(xi, np.cos(theta[:half])).ravel())         # xi_1 at nodes
+    k2 = torch.from_numpy(np.outer(xi, np.sin(theta[:half])).ravel())         # xi_2 at nodes
+    Iflat = torch.from_numpy(images.reshape(n, L * L))
+    Fh = torch.empty((n, k1.numel()), dtype=torch.complex128)
+    for s in range(0, k1.numel(), node_chunk):
+        E1 = torch.exp(-2j * math.pi * torch.outer(k1[s:s + node_chunk], idx))   # (nodes, L): e^{-2pi i xi1 i1}
+        E2 = torch.exp(-2j * math.pi * torch.outer(k2[s:s + node_chunk], idx))   # (nodes, L): e^{-2pi i xi2 i2}
+        K = (E1[:, :, None] * E2[:, None, :]).reshape(-1, L * L)               # K[node, i1 L + i2]
+        Fh[:, s:s + node_chunk] = torch.complex(Iflat @ K.real.contiguous().T,
+                                                Iflat @ K.imag.contiguous().T)
+    Fh = Fh.numpy().reshape(n, basis.n_xi, half)
     out = np.empty((n, basis.n_xi, nt), dtype=np.complex128)
-    for s in range(0, n, chunk):
-        I = images[s:s + chunk]                                   # (b, L, L) real
-        # T[b, i1, node] = sum_{i2} I[b, i1, i2] E2[node, i2]  (real x complex via 2 real GEMMs)
-        T = (I @ E2.real.T) + 1j * (I @ E2.imag.T)
-        F = np.einsum("na,ban->bn", E1, T)                        # sum over i1
-        F = F.reshape(-1, basis.n_xi, half)
-        out[s:s + chunk, :, :half] = F
-        if half != nt:
-            out[s:s + chunk, :, half:] = np.conj(F)
+    out[:, :, :half] = Fh
+    if half != nt:
+        out[:, :, half:] = np.conj(Fh)
     return out
 
 
@@ -202,12 +207,17 @@ def expand_polar(F: np.ndarray, basis: Basis, table=None) -> list:
     return radial_quadrature(angular_transform(F, basis.k_max), basis, table)
 
 
-def expand(images: np.ndarray, basis: Basis, chunk: int = 4) -> list:
-    """Algorithm 1 with the exact Fourier sum in place of the NUFFT."""
+def expand(images: np.ndarray, basis: Basis, chunk: int | None = None) -> list:
+    """Algorithm 1 with the exact Fourier sum in place of the NUFFT.
+
+    Images go through polar_ft_direct in chunks of `chunk` (default: as many as keep the polar samples of a
+    chunk near 4 GB; the dense kernel is rebuilt once per chunk, so larger chunks are faster)."""
     table = radial_table(basis)
+    if chunk is None:
+        chunk = max(1, int(4e9 // (16 * basis.n_xi * basis.n_theta)))
     parts = []
     for s in range(0, len(images), chunk):
-        F = polar_ft_direct(images[s:s + chunk], basis, chunk)
+        F = polar_ft_direct(images[s:s + chunk], basis)
         parts.append(expand_polar(F, basis, table))
     return [np.concatenate([p[k] for p in parts], axis=1) for k in range(basis.k_max + 1)]
 

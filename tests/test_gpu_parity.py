@@ -115,7 +115,7 @@ def test_expand_parity_large_L(name, n):
     plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=64)
     got = gpu_expand(plan, imgs)
     basis = O.build_basis(cfg["c"], cfg["R"])
-    ref = O.to_flat(O.expand(imgs.double().cpu().numpy(), basis, chunk=1))
+    ref = O.to_flat(O.expand(imgs.double().cpu().numpy(), basis))
     rel = rel_l2_per_image(got, ref, basis)
     assert rel.max() <= TOL32, f"{name}: {rel.max():.3e}"
 
@@ -316,7 +316,7 @@ def test_c5_full_size_sampled_expansion():
     got = coeffs[:, pick].cpu().numpy().astype(np.complex128)
     del imgs, coeffs
     basis = O.build_basis(cfg["c"], cfg["R"])
-    ref = O.to_flat(O.expand(sample, basis, chunk=1))
+    ref = O.to_flat(O.expand(sample, basis))
     rel = rel_l2_per_image(got, ref, basis)
     assert rel.max() <= TOL32, f"max per-image rel l2 {rel.max():.3e}"
 

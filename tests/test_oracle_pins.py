@@ -224,9 +224,16 @@ def test_rotation_reflection_identities_odd_L():
         assert np.max(np.abs(rot[k] - a[k] * np.exp(-1j * k * np.pi / 2))) < 1e-12 * scale
         assert np.max(np.abs(fud[k] - np.conj(a[k]))) < 1e-12 * scale
         assert np.max(np.abs(flr[k] - (-1) ** k * np.conj(a[k]))) < 1e-12 * scale
-    # rotate_coeffs / reflect_coeffs agree with those identities
+    # rotate_coeffs / reflect_coeffs agree with those identities (Eqs. (rot), (refl) P:292)
     r2 = O.rotate_coeffs(a, np.pi / 2)
     assert max(np.max(np.abs(x - y)) for x, y in zip(r2, rot)) < 1e-12 * scale
+    # reflect_coeffs(a, alpha) = conj(a) e^{-ik alpha}: alpha = 0 is the flip of axis 0 (x -> -x), alpha = pi the flip
+    # of axis 1, alpha = pi/2 the flip followed by the 90-degree rotation.  A reflect_coeffs without the conj (a
+    # rotation) or with the wrong phase sign fails at least one of the three.
+    rud = O.expand(np.rot90(I[:, ::-1, :], 1, axes=(1, 2)).copy(), b)
+    for alpha, ref in ((0.0, fud), (np.pi, flr), (np.pi / 2, rud)):
+        got = O.reflect_coeffs(a, alpha)
+        assert max(np.max(np.abs(x - y)) for x, y in zip(got, ref)) < 1e-12 * scale, alpha
 
 
 # ---------------------------------------------------------------- white noise (Fig. 3)
@@ -390,6 +397,37 @@ def test_mp_selection_and_shrinkage():
     lam_sp = (ell + s2) * (1 + gam * s2 / ell)
     h2 = O.shrink_weights([np.array([lam_sp]), np.array([lam_sp])], b, 100, s2, 2)
     assert abs(h2[1][0] - ell / (ell + s2)) < 1e-12
+
+
+def test_mp_select_edges_and_white_noise():
+    """Eq. (compselect) P:692 with gamma_0 = p_0/n, gamma_k = p_k/(2n): strict '>' at the edge, the same
+    selection shrink_weights(mode 1) makes, and on pure white noise in coefficient space (a_0 ~ N(0, s2),
+    a_k ~ CN(0, s2): C^(k) is a real Wishart with 2n samples, Marcenko-Pastur edge s2 (1 + sqrt(p_k/(2n)))^2)
+    the largest noise eigenvalue sits at the edge (a gamma_k = p_k/n slip moves the edge by 20 %), no noise
+    component is selected and a planted spike far above the BBP threshold is."""
+    b = O.Basis(c=0.5, R=1, k_max=1, p=[25, 50], zeros=[], norm=[])
+    lam = [np.array([3.0, 2.25, 2.2]), np.array([2.26, 2.25, 1.0])]
+    sel = O.mp_select(lam, b, 100, 1.0)
+    assert sel[0].tolist() == [True, False, False] and sel[1].tolist() == [True, False, False]
+    h = O.shrink_weights(lam, b, 100, 1.0, 1)
+    assert all(np.array_equal(s, hk > 0) for s, hk in zip(sel, h))
+    rng = np.random.default_rng(17)
+    p, n, s2 = 100, 500, 2.0
+    bw = O.Basis(c=0.5, R=1, k_max=1, p=[p, p], zeros=[], norm=[])
+    a0 = rng.normal(0, math.sqrt(s2), (p, n)) + 0j
+    a1 = (rng.normal(0, math.sqrt(s2 / 2), (p, n)) + 1j * rng.normal(0, math.sqrt(s2 / 2), (p, n)))
+    u = rng.standard_normal(p); u /= np.linalg.norm(u)
+    spike = (rng.normal(0, math.sqrt(5 * s2 / 2), n) + 1j * rng.normal(0, math.sqrt(5 * s2 / 2), n))
+    _, C = O.block_covariance([a0, a1])
+    lam_n, _ = O.block_eig(C)
+    edge0, edge1 = O.mp_edge(s2, p, n, 0), O.mp_edge(s2, p, n, 1)
+    assert abs(edge0 - s2 * (1 + math.sqrt(0.2)) ** 2) < 1e-12 and abs(edge1 - s2 * (1 + math.sqrt(0.1)) ** 2) < 1e-12
+    assert abs(lam_n[0][0] / edge0 - 1) < 0.05 and abs(lam_n[1][0] / edge1 - 1) < 0.05
+    assert sum(int(s.sum()) for s in O.mp_select(lam_n, bw, n, s2)) <= 1
+    _, Cs = O.block_covariance([a0, a1 + np.outer(u, spike)])
+    lam_s, _ = O.block_eig(Cs)
+    sel_s = O.mp_select(lam_s, bw, n, s2)
+    assert sel_s[1][0] and int(sel_s[1].sum()) <= 2
 
 
 def test_covariance_shard_partials_and_invariance():
