@@ -36,6 +36,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--batch", type=int, default=BATCH, help="images per expand batch (plan max_batch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nccl", action="store_true",
+                    help="use the NCCL communicator path even on one GPU (the world > 1 code path, 1 rank)")
+    ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay measurement")
     return ap.parse_args()
 
 
@@ -210,12 +213,10 @@ def main():
     plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], dtype=dt, device=local, max_batch=args.batch)
     plan.bench_batch = args.batch
     comm = None
-    if world > 1:
-        uid = torch.zeros(128, dtype=torch.uint8)
-        if rank == 0:
-            uid = torch.frombuffer(bytearray(F.fbspca_nccl_unique_id()), dtype=torch.uint8).clone()
-        obj = [uid.numpy().tobytes()]
-        dist.broadcast_object_list(obj, src=0)
+    if world > 1 or args.nccl:
+        obj = [F.fbspca_nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
         comm = F.fbspca_comm_init(obj[0], world, rank)
 
     # ---- inputs resident in HBM (generated outside the timed region; shard-invariant generator)
@@ -228,8 +229,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step():
-        F.fbspca_expand(plan, images, coeffs)
-        F.fbspca_covariance(plan, coeffs, n_local, n, comm, blocks, mean)
+        F.fbspca_step(plan, images, coeffs, blocks, mean, n, comm, use_graph=False, stream=stream)
 
     def barrier():
         torch.cuda.synchronize()
@@ -261,6 +261,30 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = t.item()
     value = n / (ms_max / 1e3)
+    if comm:
+        F.fbspca_comm_wait(comm, stream, timeout_s=60.0)     # async NCCL errors / hung peer -> abort, raise
+
+    # ---- the same step as one CUDA graph (fbspca_step use_graph: expand + K5 (both streams) + all-reduce +
+    # finalise captured once, replayed); reported beside the eager number
+    graph = None
+    if not args.no_graph:
+        gs = torch.cuda.Stream(device=dev)
+        gs.wait_stream(stream)
+        with torch.cuda.stream(gs):
+            for _ in range(3):                              # eager, capture + launch, replay
+                F.fbspca_step(plan, images, coeffs, blocks, mean, n, comm, use_graph=True, stream=gs)
+            barrier()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(gs)
+            for _ in range(args.steps):
+                F.fbspca_step(plan, images, coeffs, blocks, mean, n, comm, use_graph=True, stream=gs)
+            g1.record(gs)
+            barrier()
+        tg = torch.tensor([g0.elapsed_time(g1) / args.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+        graph = {"ms_per_step": tg.item(), "value": n / (tg.item() / 1e3), "unit": "images/s",
+                 "note": "fbspca_step with use_graph=1: one cudaGraphLaunch per step (CUDA events, max over ranks)"}
 
     # ---- e2e: same metric through the public API with HOST (pinned) inputs, H2D inside the timed region,
     # chunked and double-buffered on a copy stream, plus the D2H of the finalised blocks.
@@ -379,7 +403,11 @@ def main():
             "kernels": kernels,
             "clocks": clk,
             "gpu_launches": gpu_launches,
+            "collective": ("ncclAllReduce (in place, fp64, NCCL-registered partial buffer) over "
+                           f"{world} rank(s)" if comm else "none (1 GPU, comm = NULL)"),
         }
+        if graph:
+            line["graph"] = graph
         if e2e:
             line["e2e"] = e2e
         if cfg["name"] in PAPER_IMG_S:

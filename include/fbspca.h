@@ -30,7 +30,11 @@
  * Ownership: every pointer argument except the plan is owned by the caller.  "d_" pointers are device
  * pointers on the plan's device; all calls are asynchronous on the given stream unless stated, and a plan
  * must not be used concurrently from two streams.  The plan owns its tables and a workspace sized by
- * max_batch; no call allocates device memory.
+ * max_batch.  The hot-path calls (fbspca_expand, fbspca_covariance*, fbspca_eig, fbspca_project, fbspca_step
+ * after its first call with given arguments) allocate no device memory.  The exceptions, each stated at its
+ * declaration: the first fbspca_covariance / fbspca_step with a given communicator (NCCL-registered partial
+ * buffer), the first fbspca_synthesize (radial tables), fbspca_svd (stream-ordered workspace) and
+ * fbspca_estimate_params (not a plan call).
  *
  * Errors: every call returns fbspca_status; fbspca_last_error() returns a thread-local message.
  */
@@ -63,8 +67,11 @@ typedef enum { FBSPCA_F32 = 0, FBSPCA_F64 = 1 } fbspca_dtype;
  * Eq. (1DFFT) P:189 folded in), and the NUFFT window (width from eps) and deapodisation.
  *   L        image side (>= 4).  c band limit in (0, 1/2].  R support radius, 2 <= R <= L/2, cR >= 1.
  *            2L and n_theta must factor into 2, 3, 5, 7, 11, 13 and n_theta must be even, else FBSPCA_ERR_CONFIG.
- *   eps      NUFFT accuracy target (relative l2 of the polar samples), [1e-14, 1e-3]; <= 0 picks the
- *            default (1e-5 for F32, 1e-12 for F64).  F32 rejects eps < 1e-6.
+ *   eps      NUFFT accuracy target, [1e-14, 1e-3]; <= 0 picks the default (1e-5 for F32, 1e-12 for F64).
+ *            F32 rejects eps < 1e-6.  The window gets w = ceil(log10(1/eps)) + 1 taps per axis (F32: 6 or 7;
+ *            F64: 13) at oversampling ~2, which holds the per-image coefficient relative l2 error against
+ *            the exact Fourier sum (reading Q12) to <= max(4 eps, 4e-6) for F32 (measured 5.6e-6 at the
+ *            default 1e-5; tests/test_gpu_parity_full.py) and <= 1e-9 for F64.
  *   dt       FBSPCA_F32: images float, coefficients complex64.  FBSPCA_F64: double / complex128.
  *   device   CUDA device ordinal, or -1 for a host-only plan (census/tables only; every compute call
  *            on it returns FBSPCA_ERR_ARG).  Synchronous.
@@ -104,6 +111,21 @@ fbspca_status fbspca_expand(fbspca_plan_t plan, const void* d_images, int64_t n,
 fbspca_status fbspca_covariance(fbspca_plan_t plan, const void* d_coeffs, int64_t n_local,
                                 int64_t n_total, void* nccl_comm, double* d_blocks, double* d_mean,
                                 fbspca_stream_t stream);
+/* With a communicator, the partial buffer is the plan's NCCL buffer for that communicator (ncclMemAlloc +
+ * ncclCommRegister, NCCL >= 2.19; allocated synchronously on the first call with that communicator and
+ * released by fbspca_destroy or fbspca_comm_destroy): K5's reduction writes into it and the all-reduce runs in
+ * place on it.  After enqueueing the all-reduce the call polls ncclCommGetAsyncError; an asynchronous NCCL
+ * failure is reported as FBSPCA_ERR_NCCL. */
+
+/* One pipeline step (the bench's timed unit): fbspca_expand of n_local images into d_coeffs, then
+ * fbspca_covariance (K5, the all-reduce when nccl_comm != NULL, finalise).  use_graph != 0: the first call
+ * with a given argument set runs eagerly, the second captures the same launches (both streams of K5, the
+ * all-reduce) into one CUDA graph, and every later call with those arguments replays it with one
+ * cudaGraphLaunch; stream must then not be the legacy default stream.  Arguments as fbspca_expand and
+ * fbspca_covariance. */
+fbspca_status fbspca_step(fbspca_plan_t plan, const void* d_images, int64_t n_local, int64_t n_total,
+                          void* nccl_comm, void* d_coeffs, double* d_blocks, double* d_mean, int use_graph,
+                          fbspca_stream_t stream);
 
 /* Same as fbspca_covariance but stops before the all-reduce: writes the un-finalised partial buffer
  * (packed S_k, then s_0 (p_0 doubles), then the count) to d_partial (blk_off[k_max+1] + p_0 + 1 doubles).
@@ -172,7 +194,8 @@ fbspca_status fbspca_backproject(fbspca_plan_t plan, const void* d_c, int64_t n,
  * rho_{k,q}(r) = 2 c sqrt(pi) (-1)^q R_{k,q} J_k(2 pi c r) / ((2 pi c r)^2 - R_{k,q}^2) (q = 1..p_k), for pixels with
  * r <= R (zero elsewhere, the compact support P:115); axis 0 = i1 (Q3).  fp64 arithmetic.  d_coeffs: coefficient
  * layout, ld = n.  d_images: n x L x L (float or double per dt), n <= 65535 per call.  The first call builds
- * the plan's radial tables (host, synchronous).  Asynchronous otherwise. */
+ * the plan's radial tables on the host and uploads them (cudaMalloc + synchronous copies: the one allocating
+ * call of the synthesis path).  Asynchronous otherwise. */
 fbspca_status fbspca_synthesize(fbspca_plan_t plan, const void* d_coeffs, int64_t n, void* d_images,
                                 fbspca_stream_t stream);
 
@@ -190,10 +213,17 @@ fbspca_status fbspca_synthesize(fbspca_plan_t plan, const void* d_coeffs, int64_
 fbspca_status fbspca_estimate_params(int L, fbspca_dtype dt, int device, const void* d_images, int64_t n,
                                      double fraction, double* sigma2, double* R, double* c);
 
-/* NCCL plumbing (libnccl.so.2 is dlopen'ed on first use).  unique_id: 128 bytes. */
+/* NCCL plumbing (libnccl.so.2 is dlopen'ed on first use).  unique_id: 128 bytes.  fbspca_comm_destroy first
+ * releases the plans' registered buffers for that communicator. */
 fbspca_status fbspca_nccl_unique_id(void* unique_id_out);
 fbspca_status fbspca_comm_init(const void* unique_id, int nranks, int rank, void** nccl_comm_out);
 fbspca_status fbspca_comm_destroy(void* nccl_comm);
+
+/* Failure detection: wait for `stream` while polling ncclCommGetAsyncError every 100 us.
+ * Returns FBSPCA_OK when the stream's work is done; on an asynchronous NCCL error, or when timeout_s > 0
+ * seconds pass first (a hung peer), aborts the communicator (ncclCommAbort) and returns FBSPCA_ERR_NCCL
+ * naming the cause.  Synchronous. */
+fbspca_status fbspca_comm_wait(void* nccl_comm, fbspca_stream_t stream, double timeout_s);
 
 /* Per-kernel-family device times when timing is on (CUDA events recorded around each launch on the
  * call's stream; off by default).  fbspca_get_timing synchronises those events, returns *count family

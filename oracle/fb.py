@@ -140,35 +140,43 @@ def radial_table(basis: Basis, xi=None, w=None):
 # O5 direct Fourier sum at the polar nodes (Eq. (nufft); Q1 unit prefactor)
 # --------------------------------------------------------------------------
 def polar_ft_direct(images: np.ndarray, basis: Basis, chunk: int | None = None,
-                    node_chunk: int = 1024) -> np.ndarray:
+                    node_chunk: int = 1024, dense: bool | None = None) -> np.ndarray:
     """F(I)(xi_1, xi_2) = sum_{i1,i2} I(i1,i2) exp(-2 pi i (xi_1 i1 + xi_2 i2))   (Eq. (nufft), Q1 unit prefactor).
 
-    Evaluated exactly (up to rounding) at every node (xi_j cos theta_l, xi_j sin theta_l) as one matrix
-    product F = I_flat K^T with the dense kernel K[node, (i1, i2)] = e^{-2 pi i xi_1 i1} e^{-2 pi i xi_2 i2}
-    (built per block of node_chunk nodes; fp64 BLAS through torch).  Nodes l < n_theta/2 are summed directly;
-    for even n_theta the node l + n_theta/2 is the negated node l, where the sum for a real image is the
-    complex conjugate (exact identity of the definition for real I).  `chunk` is accepted for
-    compatibility and ignored (all images go through each kernel block at once).
-    Returns (n, n_xi, n_theta) complex128.
+    Evaluated exactly (up to rounding) at every node (xi_j cos theta_l, xi_j sin theta_l), with
+    E1[node, i1] = e^{-2 pi i xi_1 i1} and E2[node, i2] = e^{-2 pi i xi_2 i2}, in one of two orders of the same
+    double sum (fp64 BLAS through torch, per block of node_chunk nodes):
+      dense     (default for n >= 32): F = I_flat K^T with the dense kernel K[node, i1 L + i2] = E1 E2;
+      separable (small n):            T[i1, node] = sum_{i2} I[i1, i2] E2[node, i2], F = sum_{i1} E1[node, i1] T.
+    Nodes l < n_theta/2 are summed directly; for even n_theta the node l + n_theta/2 is the negated node l,
+    where the sum for a real image is the complex conjugate (exact identity of the definition for real I,
+    P:197).  `chunk` is accepted for compatibility and ignored.  Returns (n, n_xi, n_theta) complex128.
     """
     import torch
     images = np.asarray(images, dtype=np.float64)
     n, L, L2 = images.shape
     assert L == L2
+    if dense is None:
+        dense = n >= 32
     xi, _, theta = polar_grid(basis)
     nt = basis.n_theta
     half = nt // 2 if nt % 2 == 0 else nt
     idx = torch.arange(L, dtype=torch.float64) - L // 2                       # i = a - floor(L/2)
     k1 = torch.from_numpy(np.outer(xi, np.cos(theta[:half])).ravel())         # xi_1 at nodes
     k2 = torch.from_numpy(np.outer(xi, np.sin(theta[:half])).ravel())         # xi_2 at nodes
-    Iflat = torch.from_numpy(images.reshape(n, L * L))
+    I3 = torch.from_numpy(images)
     Fh = torch.empty((n, k1.numel()), dtype=torch.complex128)
     for s in range(0, k1.numel(), node_chunk):
         E1 = torch.exp(-2j * math.pi * torch.outer(k1[s:s + node_chunk], idx))   # (nodes, L): e^{-2pi i xi1 i1}
         E2 = torch.exp(-2j * math.pi * torch.outer(k2[s:s + node_chunk], idx))   # (nodes, L): e^{-2pi i xi2 i2}
-        K = (E1[:, :, None] * E2[:, None, :]).reshape(-1, L * L)               # K[node, i1 L + i2]
-        Fh[:, s:s + node_chunk] = torch.complex(Iflat @ K.real.contiguous().T,
-                                                Iflat @ K.imag.contiguous().T)
+        if dense:
+            K = (E1[:, :, None] * E2[:, None, :]).reshape(-1, L * L)           # K[node, i1 L + i2]
+            If = I3.reshape(n, L * L)
+            Fh[:, s:s + node_chunk] = torch.complex(If @ K.real.contiguous().T, If @ K.imag.contiguous().T)
+        else:
+            for b in range(n):
+                T = torch.complex(I3[b] @ E2.real.T.contiguous(), I3[b] @ E2.imag.T.contiguous())  # (i1, node)
+                Fh[b, s:s + node_chunk] = (E1.T * T).sum(0)
     Fh = Fh.numpy().reshape(n, basis.n_xi, half)
     out = np.empty((n, basis.n_xi, nt), dtype=np.complex128)
     out[:, :, :half] = Fh

@@ -40,6 +40,9 @@ SIGNATURES = {
     "fbspca_nccl_unique_id": (c_int, [c_void_p]),
     "fbspca_comm_init": (c_int, [c_void_p, c_int, c_int, ctypes.POINTER(c_void_p)]),
     "fbspca_comm_destroy": (c_int, [c_void_p]),
+    "fbspca_comm_wait": (c_int, [c_void_p, c_void_p, c_double]),
+    "fbspca_step": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
+                            c_void_p]),
     "fbspca_set_timing": (c_int, [c_void_p, c_int]),
     "fbspca_get_timing": (c_int, [c_void_p, P_int, ctypes.POINTER(ctypes.POINTER(c_char_p)),
                                   ctypes.POINTER(ctypes.POINTER(ctypes.c_float))]),

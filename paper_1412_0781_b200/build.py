@@ -1,6 +1,12 @@
-"""Build libfbspca.so in-tree with nvcc for sm_100a (no JIT, no torch extension machinery)."""
+"""Build libfbspca.so in-tree with nvcc for sm_100a (no JIT, no torch extension machinery).
+
+Staleness is decided by content, not mtimes: every object has a sidecar with the SHA-256 of its source, the
+shared headers and the flags; the library has a sidecar with the hash of all sources (also compiled into
+fbspca_version(), so a loaded library names the sources it was built from).  A pushed prebuilt .so whose
+sidecar does not match the tree is rebuilt."""
 from __future__ import annotations
 
+import hashlib
 import os
 import subprocess
 import sys
@@ -16,11 +22,26 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
 
 
-def _stale(target: str, deps: list[str]) -> bool:
-    if not os.path.exists(target):
-        return True
-    t = os.path.getmtime(target)
-    return any(os.path.getmtime(d) > t for d in deps)
+def _digest(paths, extra=()) -> str:
+    h = hashlib.sha256()
+    for p in paths:
+        h.update(os.path.basename(p).encode())
+        h.update(open(p, "rb").read())
+    for e in extra:
+        h.update(e.encode())
+    return h.hexdigest()[:16]
+
+
+def source_hash() -> str:
+    """Hash of every source and header the library is built from (and the flags)."""
+    return _digest([os.path.join(PKG, s) for s in SRC] + [os.path.join(PKG, h) for h in HDR], FLAGS)
+
+
+def _sidecar(path: str) -> str | None:
+    try:
+        return open(path + ".hash").read().strip()
+    except OSError:
+        return None
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -28,24 +49,31 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     hdrs = [os.path.join(PKG, h) for h in HDR]
+    shash = source_hash()
+    if not force and os.path.exists(LIB) and _sidecar(LIB) == shash:
+        return LIB                       # built from exactly these sources (objects need not be present)
     procs, objs = [], []
     for s in SRC:
         src = os.path.join(PKG, s)
         obj = os.path.join(objdir, os.path.basename(s) + ".o")
         objs.append(obj)
-        if force or _stale(obj, [src] + hdrs):
-            cmd = [NVCC] + FLAGS + ["-c", src, "-o", obj]
+        flags = FLAGS + ([f'-DFBSPCA_SRC_HASH="{shash}"'] if s.endswith("capi.cu") else [])
+        want = _digest([src] + hdrs, flags)
+        if force or not os.path.exists(obj) or _sidecar(obj) != want:
+            cmd = [NVCC] + flags + ["-c", src, "-o", obj]
             log = open(obj + ".log", "w")
-            procs.append((s, subprocess.Popen(cmd, stdout=log, stderr=subprocess.STDOUT), obj + ".log"))
-    for s, p, logf in procs:
+            procs.append((s, subprocess.Popen(cmd, stdout=log, stderr=subprocess.STDOUT), obj, want))
+    for s, p, obj, want in procs:
         if p.wait() != 0:
-            sys.stderr.write(open(logf).read())
-            raise RuntimeError(f"nvcc failed on {s}; see {logf}")
+            sys.stderr.write(open(obj + ".log").read())
+            raise RuntimeError(f"nvcc failed on {s}; see {obj}.log")
+        open(obj + ".hash", "w").write(want + "\n")
         if verbose:
-            sys.stdout.write(open(logf).read())
-    if force or procs or _stale(LIB, objs):
+            sys.stdout.write(open(obj + ".log").read())
+    if force or procs or not os.path.exists(LIB) or _sidecar(LIB) != shash:
         cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs + ["-ldl"]
         subprocess.check_call(cmd)
+        open(LIB + ".hash", "w").write(shash + "\n")
     return LIB
 
 

@@ -4,7 +4,11 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <map>
+#include <mutex>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -16,6 +20,22 @@ namespace fbspca {
 
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies per device: remember what was set per (kernel, device)
+// under a mutex so a plan on a second device (or another thread) gets its own opt-in.
+cudaError_t ensure_smem_optin(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = done[{func, dev}];
+  if (have >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
 
 namespace {
 
@@ -67,13 +87,25 @@ enum TimingKind { T_POLAR = 0, T_RADIAL, T_COV, T_ALLREDUCE, T_FINALIZE, T_EIG, 
 const char* kTimingNames[T_NKINDS] = {"polar_K1K2K3", "radial_K4", "cov_K5", "allreduce", "finalize", "eig_K6",
                                       "project_K7"};
 
+// Events come from a per-plan pool (created once, reused after every fbspca_get_timing), so a timed region costs
+// two cudaEventRecord calls and no event creation.  Regions inside a stream capture are not timed.
 struct TimedRegion {
-  Plan& P; int kind; cudaStream_t s; cudaEvent_t e0 = nullptr, e1 = nullptr;
+  Plan& P; int kind; cudaStream_t s; bool on = false; cudaEvent_t e0 = nullptr, e1 = nullptr;
   TimedRegion(Plan& p, int kd, cudaStream_t st) : P(p), kind(kd), s(st) {
-    if (P.timing) { cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventRecord(e0, s); }
+    if (!P.timing) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+    const size_t need = 2 * (P.tevents.size() + 1);
+    while (P.event_pool.size() < need) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return;
+      P.event_pool.push_back(e);
+    }
+    e0 = P.event_pool[need - 2]; e1 = P.event_pool[need - 1];
+    on = cudaEventRecord(e0, s) == cudaSuccess;
   }
   ~TimedRegion() {
-    if (P.timing) { cudaEventRecord(e1, s); P.tevents.push_back({kind, {e0, e1}}); }
+    if (on && cudaEventRecord(e1, s) == cudaSuccess) P.tevents.push_back({kind, {e0, e1}});
   }
 };
 
@@ -85,6 +117,13 @@ struct Nccl {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  // optional (NCCL >= 2.19): NCCL-allocated, communicator-registered buffers; async error query / abort
+  ncclResult_t (*MemAlloc)(void**, size_t) = nullptr;
+  ncclResult_t (*MemFree)(void*) = nullptr;
+  ncclResult_t (*CommRegister)(ncclComm_t, void*, size_t, void**) = nullptr;
+  ncclResult_t (*CommDeregister)(ncclComm_t, void*) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
 };
 Nccl g_nccl;
 
@@ -99,6 +138,12 @@ bool nccl_load() {
   g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
   g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
   g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+  g_nccl.MemAlloc = (decltype(g_nccl.MemAlloc))dlsym(h, "ncclMemAlloc");
+  g_nccl.MemFree = (decltype(g_nccl.MemFree))dlsym(h, "ncclMemFree");
+  g_nccl.CommRegister = (decltype(g_nccl.CommRegister))dlsym(h, "ncclCommRegister");
+  g_nccl.CommDeregister = (decltype(g_nccl.CommDeregister))dlsym(h, "ncclCommDeregister");
+  g_nccl.CommGetAsyncError = (decltype(g_nccl.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+  g_nccl.CommAbort = (decltype(g_nccl.CommAbort))dlsym(h, "ncclCommAbort");
   g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.CommDestroy;
   if (!g_nccl.ok) set_error("libnccl.so.2 lacks required symbols");
   return g_nccl.ok;
@@ -107,6 +152,65 @@ bool nccl_load() {
 fbspca_status nccl_fail(ncclResult_t r, const char* where) {
   set_error(std::string(where) + ": " + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "nccl error"));
   return FBSPCA_ERR_NCCL;
+}
+
+// Errors NCCL raised asynchronously on a communicator (a peer died, a network failure): polled after every
+// collective this library enqueues and by fbspca_comm_wait.
+fbspca_status nccl_async_check(ncclComm_t comm, const char* where) {
+  if (!g_nccl.CommGetAsyncError) return FBSPCA_OK;
+  ncclResult_t st = ncclSuccess;
+  ncclResult_t r = g_nccl.CommGetAsyncError(comm, &st);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclCommGetAsyncError");
+  if (st != ncclSuccess && st != ncclInProgress) return nccl_fail(st, where);
+  return FBSPCA_OK;
+}
+
+// The plans' NCCL-visible partial buffers (SURVEY 8(e) Level 1): allocated with ncclMemAlloc and registered with
+// the communicator on first use, so K5's chunk reduction writes straight into the buffer the in-place all-reduce
+// reads (no staging copy).  Keyed by (plan, comm); released by fbspca_destroy or fbspca_comm_destroy, whichever
+// comes first.
+struct RegBuf { void* ptr = nullptr; void* handle = nullptr; size_t bytes = 0; };
+std::mutex g_reg_mu;
+std::map<std::pair<Plan*, void*>, RegBuf> g_reg;
+
+void release_regbuf(std::pair<Plan*, void*> key, RegBuf& b) {
+  if (b.handle && g_nccl.CommDeregister) g_nccl.CommDeregister((ncclComm_t)key.second, b.handle);
+  if (b.ptr) { if (g_nccl.MemFree) g_nccl.MemFree(b.ptr); else cudaFree(b.ptr); }
+  b = RegBuf{};
+}
+
+// Partial buffer for (plan, comm): registered if this NCCL supports it, else the plan's own buffer.
+fbspca_status registered_partial(Plan& P, void* comm, double** out) {
+  *out = P.d_partial;
+  if (!comm || !g_nccl.MemAlloc || !g_nccl.CommRegister) return FBSPCA_OK;
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  RegBuf& b = g_reg[{&P, comm}];
+  const size_t bytes = (size_t)(P.blk_off[P.k_max + 1] + P.p[0] + 1) * sizeof(double);
+  if (!b.ptr) {
+    ncclResult_t r = g_nccl.MemAlloc(&b.ptr, bytes);
+    if (r != ncclSuccess) { b = RegBuf{}; return nccl_fail(r, "ncclMemAlloc"); }
+    r = g_nccl.CommRegister((ncclComm_t)comm, b.ptr, bytes, &b.handle);
+    if (r != ncclSuccess) { g_nccl.MemFree(b.ptr); b = RegBuf{}; return nccl_fail(r, "ncclCommRegister"); }
+    b.bytes = bytes;
+  }
+  *out = static_cast<double*>(b.ptr);
+  return FBSPCA_OK;
+}
+
+void release_plan_regbufs(Plan* P) {
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  for (auto it = g_reg.begin(); it != g_reg.end();) {
+    if (it->first.first == P) { release_regbuf(it->first, it->second); it = g_reg.erase(it); }
+    else ++it;
+  }
+}
+
+void release_comm_regbufs(void* comm) {
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  for (auto it = g_reg.begin(); it != g_reg.end();) {
+    if (it->first.second == comm) { release_regbuf(it->first, it->second); it = g_reg.erase(it); }
+    else ++it;
+  }
 }
 
 fbspca_status upload_plan(Plan& P) {
@@ -198,7 +302,11 @@ void free_plan(Plan& P) {
                   P.d_synth_rho, P.d_synth_pidx, P.d_synth_pir, P.d_synth_pcs, P.d_synth_grp,
                   P.d_noderec, P.d_dnoderec};
   for (void* p : ptrs) if (p) cudaFree(p);
-  for (auto& ev : P.tevents) { cudaEventDestroy(ev.second.first); cudaEventDestroy(ev.second.second); }
+  for (cudaEvent_t e : P.event_pool) cudaEventDestroy(e);
+  P.event_pool.clear();
+  P.tevents.clear();
+  for (auto& g : P.graphs) if (g.exec) cudaGraphExecDestroy(g.exec);
+  P.graphs.clear();
   if (P.ev_fork) cudaEventDestroy(P.ev_fork);
   if (P.ev_join) cudaEventDestroy(P.ev_join);
   if (P.side) cudaStreamDestroy(P.side);
@@ -222,7 +330,10 @@ extern "C" {
 struct fbspca_plan_s : public fbspca::Plan {};
 
 const char* fbspca_last_error(void) { return g_err.c_str(); }
-const char* fbspca_version(void) { return "fbspca-b200 0.1 (sm_100a)"; }
+#ifndef FBSPCA_SRC_HASH
+#define FBSPCA_SRC_HASH "unknown"
+#endif
+const char* fbspca_version(void) { return "fbspca-b200 0.2 (sm_100a) src " FBSPCA_SRC_HASH; }
 
 fbspca_status fbspca_plan(int L, double c, double R, double eps, fbspca_dtype dt, int device, int64_t max_batch,
                           fbspca_plan_t* out) {
@@ -286,7 +397,9 @@ fbspca_status fbspca_expand(fbspca_plan_t h, const void* d_images, int64_t n, vo
     }
     {
       TimedRegion t(P, T_RADIAL, s);
-      if (P.dt == FBSPCA_F32 && P.use_tc && P.n_xi % 4 == 0) FB_CUDA(launch_radial_tma(P, nb, b0, n, d_coeffs, s), "radial tma kernel");
+      // tensor-core K4 takes p_0 <= 256 (its B tiles); larger bases (c R > ~80) run the SIMT kernel
+      if (P.dt == FBSPCA_F32 && P.use_tc && P.n_xi % 4 == 0 && ((P.p[0] + 15) & ~15) <= 256)
+        FB_CUDA(launch_radial_tma(P, nb, b0, n, d_coeffs, s), "radial tma kernel");
       else FB_CUDA(launch_radial(P, nb, b0, n, d_coeffs, s), "radial kernel");
     }
   }
@@ -334,10 +447,12 @@ fbspca_status fbspca_allreduce_partial(fbspca_plan_t h, double* d_partial, void*
   DeviceGuard g(P.device);
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t npart = P.blk_off[P.k_max + 1] + P.p[0] + 1;
-  TimedRegion t(P, T_ALLREDUCE, s);
-  ncclResult_t r = g_nccl.AllReduce(d_partial, d_partial, (size_t)npart, ncclFloat64, ncclSum, (ncclComm_t)nccl_comm, s);
-  if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
-  return FBSPCA_OK;
+  {
+    TimedRegion t(P, T_ALLREDUCE, s);
+    ncclResult_t r = g_nccl.AllReduce(d_partial, d_partial, (size_t)npart, ncclFloat64, ncclSum, (ncclComm_t)nccl_comm, s);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
+  }
+  return nccl_async_check((ncclComm_t)nccl_comm, "ncclAllReduce (async)");
 }
 
 fbspca_status fbspca_covariance_finalize(fbspca_plan_t h, const double* d_partial, double* d_blocks, double* d_mean,
@@ -360,11 +475,57 @@ fbspca_status fbspca_covariance(fbspca_plan_t h, const void* d_coeffs, int64_t n
   Plan& P = *h;
   if (n_total < n_local) { set_error("n_total < n_local"); return FBSPCA_ERR_ARG; }
   if (!nccl_comm && n_total != n_local) { set_error("n_total != n_local without a communicator"); return FBSPCA_ERR_ARG; }
-  st = fbspca_covariance_partial(h, d_coeffs, n_local, P.d_partial, stream);
+  double* part = P.d_partial;
+  if (nccl_comm) {
+    if (!nccl_load()) return FBSPCA_ERR_NCCL;
+    DeviceGuard g(P.device);
+    st = registered_partial(P, nccl_comm, &part);       // K5 writes straight into the all-reduce buffer
+    if (st != FBSPCA_OK) return st;
+  }
+  st = fbspca_covariance_partial(h, d_coeffs, n_local, part, stream);
   if (st != FBSPCA_OK) return st;
-  st = fbspca_allreduce_partial(h, P.d_partial, nccl_comm, stream);
+  st = fbspca_allreduce_partial(h, part, nccl_comm, stream);
   if (st != FBSPCA_OK) return st;
-  return fbspca_covariance_finalize(h, P.d_partial, d_blocks, d_mean, stream);
+  return fbspca_covariance_finalize(h, part, d_blocks, d_mean, stream);
+}
+
+fbspca_status fbspca_step(fbspca_plan_t h, const void* d_images, int64_t n_local, int64_t n_total, void* nccl_comm,
+                          void* d_coeffs, double* d_blocks, double* d_mean, int use_graph, fbspca_stream_t stream) {
+  fbspca_status st = check_compute_plan(h);
+  if (st != FBSPCA_OK) return st;
+  Plan& P = *h;
+  cudaStream_t s = (cudaStream_t)stream;
+  auto eager = [&]() -> fbspca_status {
+    fbspca_status r = fbspca_expand(h, d_images, n_local, d_coeffs, stream);
+    if (r != FBSPCA_OK) return r;
+    return fbspca_covariance(h, d_coeffs, n_local, n_total, nccl_comm, d_blocks, d_mean, stream);
+  };
+  if (!use_graph) return eager();
+  if (!s) { set_error("step: graph capture needs a non-default stream"); return FBSPCA_ERR_ARG; }
+  DeviceGuard g(P.device);
+  Plan::GraphEntry* ge = nullptr;
+  for (auto& e : P.graphs)
+    if (e.images == d_images && e.n_local == n_local && e.n_total == n_total && e.comm == nccl_comm &&
+        e.coeffs == d_coeffs && e.blocks == d_blocks && e.mean == d_mean && e.stream == s) { ge = &e; break; }
+  if (!ge) {
+    P.graphs.push_back({d_images, n_local, n_total, nccl_comm, d_coeffs, d_blocks, d_mean, s, 0, nullptr});
+    ge = &P.graphs.back();
+  }
+  if (ge->uses++ == 0) return eager();       // first call: eager (kernel attributes, NCCL registration happen here)
+  if (!ge->exec) {                           // second call: capture the same launches into one graph
+    FB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed), "begin capture");
+    fbspca_status r = eager();
+    cudaGraph_t graph = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(s, &graph);
+    if (r != FBSPCA_OK) { if (graph) cudaGraphDestroy(graph); return r; }
+    if (ce != cudaSuccess) return cuda_fail(ce, "end capture");
+    ce = cudaGraphInstantiate(&ge->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) { ge->exec = nullptr; return cuda_fail(ce, "graph instantiate"); }
+  }
+  FB_CUDA(cudaGraphLaunch(ge->exec, s), "graph launch");
+  if (nccl_comm) return nccl_async_check((ncclComm_t)nccl_comm, "graph all-reduce (async)");
+  return FBSPCA_OK;
 }
 
 fbspca_status fbspca_eig(fbspca_plan_t h, const double* d_blocks, double* d_evals, double* d_evecs,
@@ -515,9 +676,33 @@ fbspca_status fbspca_comm_init(const void* uid, int nranks, int rank, void** com
   return FBSPCA_OK;
 }
 
+fbspca_status fbspca_comm_wait(void* comm, fbspca_stream_t stream, double timeout_s) {
+  if (!comm) { set_error("comm_wait: null communicator"); return FBSPCA_ERR_ARG; }
+  if (!nccl_load()) return FBSPCA_ERR_NCCL;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    fbspca_status st = nccl_async_check((ncclComm_t)comm, "NCCL (async)");
+    if (st != FBSPCA_OK) {
+      if (g_nccl.CommAbort) g_nccl.CommAbort((ncclComm_t)comm);
+      return st;
+    }
+    cudaError_t q = cudaStreamQuery((cudaStream_t)stream);
+    if (q == cudaSuccess) return FBSPCA_OK;
+    if (q != cudaErrorNotReady) return cuda_fail(q, "comm_wait: stream");
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (timeout_s > 0 && el > timeout_s) {
+      if (g_nccl.CommAbort) g_nccl.CommAbort((ncclComm_t)comm);
+      set_error("comm_wait: stream not done after " + std::to_string(timeout_s) + " s; communicator aborted");
+      return FBSPCA_ERR_NCCL;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(100));
+  }
+}
+
 fbspca_status fbspca_comm_destroy(void* comm) {
   if (!comm) return FBSPCA_OK;
   if (!nccl_load()) return FBSPCA_ERR_NCCL;
+  release_comm_regbufs(comm);
   ncclResult_t r = g_nccl.CommDestroy((ncclComm_t)comm);
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
   return FBSPCA_OK;
@@ -539,7 +724,6 @@ fbspca_status fbspca_get_timing(fbspca_plan_t h, int* count, const char* const**
     cudaEventElapsedTime(&t, ev.second.first, ev.second.second);
     P.tms[ev.first] += t;
     P.tms[T_NKINDS + ev.first] += 1.f;
-    cudaEventDestroy(ev.second.first); cudaEventDestroy(ev.second.second);
   }
   P.tevents.clear();
   P.tname_ptrs.assign(kTimingNames, kTimingNames + T_NKINDS);
@@ -551,6 +735,7 @@ fbspca_status fbspca_get_timing(fbspca_plan_t h, int* count, const char* const**
 
 void fbspca_destroy(fbspca_plan_t h) {
   if (!h) return;
+  release_plan_regbufs(h);
   free_plan(*h);
   delete h;
 }

@@ -108,6 +108,17 @@ template <int GS> __device__ __forceinline__ void gsync(int bar) {
   else asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(GS) : "memory");
 }
 
+// w[r] = w[1]^r, r = 2..R-1, from w[1] by at most three multiplications deep
+template <typename T2, int R>
+__device__ __forceinline__ void twiddle_powers(T2* w) {
+  if constexpr (R > 2) w[2] = cmul(w[1], w[1]);
+  if constexpr (R > 3) w[3] = cmul(w[1], w[2]);
+  if constexpr (R > 4) w[4] = cmul(w[2], w[2]);
+  if constexpr (R > 5) w[5] = cmul(w[1], w[4]);
+  if constexpr (R > 6) w[6] = cmul(w[2], w[4]);
+  if constexpr (R > 7) w[7] = cmul(w[3], w[4]);
+}
+
 template <typename T2, int N, int R, int Ns, int TOFF, bool HZ = false, int GS = 32, class Ld, class St>
 __device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tws, int lane, int bar = 0) {
   constexpr int NB = N / R;
@@ -122,7 +133,15 @@ __device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tws,
         else v[r] = ld(j + r * NB);
       }
       const int jm = j % Ns;                      // compile-time Ns: a mask for powers of two
-      if constexpr (Ns > 1) {
+      if constexpr (Ns > 1 && sizeof(v[0].x) == 4 && R >= 3) {
+        // fp32: one table load per butterfly; w^r for r >= 2 by products of w (depth <= 3 multiplications,
+        // relative error <= ~4e-7, below the fp32 FFT's own ~log2(N) u).  Saves R - 2 shared loads.
+        T2 w[R];
+        w[1] = tws[TOFF + jm];
+        twiddle_powers<T2, R>(w);
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], w[r]);
+      } else if constexpr (Ns > 1) {
 #pragma unroll
         for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tws[TOFF + (r - 1) * Ns + jm]);
       }

@@ -126,6 +126,13 @@ struct Plan {
   std::vector<const char*> tname_ptrs;
   std::vector<float> tms;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> tevents;
+  std::vector<cudaEvent_t> event_pool;   // timing events, created once and reused
+  // fbspca_step CUDA graphs: one instantiated graph per argument set (pointers, counts, communicator, stream)
+  struct GraphEntry {
+    const void* images; int64_t n_local, n_total; void* comm; void* coeffs; double* blocks; double* mean;
+    cudaStream_t stream; int uses; cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs;
   int num_sms = 0;
   // NEXT-1 synthesis tables (built on the first fbspca_synthesize)
   double* d_synth_rho = nullptr;         // [coef row][radius]: rho_{k,q}(r)
@@ -137,6 +144,9 @@ struct Plan {
   cudaStream_t side = nullptr;           // K5: the k = 0 fp64 CTAs run here, forked from / joined to the caller's stream
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
+
+// per-(kernel, device) dynamic shared-memory opt-in, thread-safe (capi.cu)
+cudaError_t ensure_smem_optin(const void* func, int bytes);
 
 // ---- host plan construction (plan.cpp) ----
 fbspca_status build_host_plan(Plan& P);           // census, grid, table, NUFFT, phases (no CUDA)

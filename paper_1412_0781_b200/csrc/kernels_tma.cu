@@ -547,12 +547,8 @@ cudaError_t launch_radial_tma(const Plan& P, int64_t nb, int64_t i0, int64_t ld,
   const int budget = (per_sm == 2 ? 113 : 227) * 1024;
   a.stages = std::max(2, std::min(8, (budget - fixed) / stage));
   const int smem = a.stages * stage + fixed;
-  static int configured = 0;
-  if (configured < smem) {
-    cudaError_t e = cudaFuncSetAttribute(radial_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(radial_tma_kernel), smem);
+  if (e != cudaSuccess) return e;
   const int items = nk * a.nrt;
   const int grid = std::min(items, per_sm * P.num_sms);
   radial_tma_kernel<<<grid, 320, smem, s>>>(ta, tbh, tbl, a);
@@ -570,12 +566,8 @@ static cudaError_t launch_cov_tma_t(const Plan& P, const MapSet& ta, K5Args& a, 
   const int stage = a.ck * std::max(128, 2 * RR) * ROWB;
   a.stages = std::max(2, std::min(8, (budget - fixed) / stage));
   const int smem = a.stages * stage + fixed;
-  static int configured = 0;
-  if (configured < smem) {
-    cudaError_t e = cudaFuncSetAttribute(cov_tma_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(cov_tma_kernel<RR>), smem);
+  if (e != cudaSuccess) return e;
   const int items = a.k_max * a.nchunk;
   const int grid = std::min(items, per_sm * P.num_sms);
   cov_tma_kernel<RR><<<grid, 192, smem, s>>>(ta, a);

@@ -257,7 +257,7 @@ fbspca_status build_host_plan(Plan& P) {
   while (!smooth5(M) || M % 2) ++M;
   P.M = M;
   int w = int(std::ceil(-std::log10(P.eps) - 1e-9)) + 1;         // error ~ 10^{-(w-1)} at sigma = 2
-  if (P.dt == FBSPCA_F32) { w = std::max(6, std::min(w, 8)); }
+  if (P.dt == FBSPCA_F32) { w = std::max(6, std::min(w, 7)); }   // eps >= 1e-6 (fp32 floor) -> w <= 7
   else { w = std::max(w, 13); if (w > 13) w = 13; }
   P.w = w;
   P.beta = 2.30 * w;

@@ -112,13 +112,29 @@ def fbspca_plan(L: int, c: float, R: float, eps: float = 0.0, dtype: int = F32, 
                 wq=np.ctypeslib.as_array(wp, shape=(n_xi.value,)).copy())
 
 
+def _on_plan_device(plan: Plan, *tensors):
+    for t in tensors:
+        if t.device.type != "cuda" or t.device.index != plan.device:
+            raise FbspcaError(f"tensor on {t.device}, plan on cuda:{plan.device}")
+
+
+def _check_coeffs(plan: Plan, coeffs: torch.Tensor, n: int, what: str = "coeffs"):
+    """The C ABI takes ld = n: a (n_coef, n) complex tensor of the plan's precision, contiguous."""
+    if tuple(coeffs.shape) != (plan.n_coef, n) or coeffs.dtype != plan.complex_dtype:
+        raise FbspcaError(f"{what} must be ({plan.n_coef}, {n}) {plan.complex_dtype}, got {tuple(coeffs.shape)} "
+                          f"{coeffs.dtype}")
+
+
 def fbspca_expand(plan: Plan, images: torch.Tensor, coeffs: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """images (n, L, L) on the plan's device -> coefficients (n_coef, n) complex (coefficient layout)."""
     n = images.shape[0]
     if images.dtype != plan.real_dtype or tuple(images.shape[1:]) != (plan.L, plan.L):
         raise FbspcaError(f"images must be (n, {plan.L}, {plan.L}) {plan.real_dtype}")
+    _on_plan_device(plan, images)
     if coeffs is None:
         coeffs = torch.empty((plan.n_coef, n), dtype=plan.complex_dtype, device=images.device)
+    _check_coeffs(plan, coeffs, n)
+    _on_plan_device(plan, coeffs)
     check(lib().fbspca_expand(ctypes.c_void_p(plan.handle), _ptr(images), n, _ptr(coeffs), _stream_ptr(stream)),
           "fbspca_expand")
     return coeffs
@@ -128,6 +144,8 @@ def fbspca_covariance(plan: Plan, coeffs: torch.Tensor, n_local: int | None = No
                       comm: int | None = None, blocks=None, mean=None, stream=None):
     n_local = coeffs.shape[1] if n_local is None else n_local
     n_total = n_local if n_total is None else n_total
+    _check_coeffs(plan, coeffs, n_local)
+    _on_plan_device(plan, coeffs)
     dev = coeffs.device
     if blocks is None:
         blocks = torch.empty(plan.n_blk, dtype=torch.float64, device=dev)
@@ -140,6 +158,7 @@ def fbspca_covariance(plan: Plan, coeffs: torch.Tensor, n_local: int | None = No
 
 
 def fbspca_covariance_partial(plan: Plan, coeffs: torch.Tensor, partial=None, stream=None) -> torch.Tensor:
+    _check_coeffs(plan, coeffs, coeffs.shape[1])
     if partial is None:
         partial = torch.empty(plan.n_partial, dtype=torch.float64, device=coeffs.device)
     check(lib().fbspca_covariance_partial(ctypes.c_void_p(plan.handle), _ptr(coeffs), coeffs.shape[1], _ptr(partial),
@@ -236,6 +255,23 @@ def fbspca_project(plan: Plan, coeffs: torch.Tensor, mean, evals, evecs, sigma2:
                                float(sigma2), int(mode), int(n_total), _ptr(out), _stream_ptr(stream)),
           "fbspca_project")
     return out
+
+
+def fbspca_step(plan: Plan, images: torch.Tensor, coeffs: torch.Tensor, blocks: torch.Tensor, mean: torch.Tensor,
+                n_total: int | None = None, comm: int | None = None, use_graph: bool = False, stream=None):
+    """expand + covariance (+ all-reduce) + finalise as one call; use_graph replays a captured CUDA graph."""
+    n = images.shape[0]
+    n_total = n if n_total is None else n_total
+    _check_coeffs(plan, coeffs, n)
+    _on_plan_device(plan, images, coeffs, blocks, mean)
+    check(lib().fbspca_step(ctypes.c_void_p(plan.handle), _ptr(images), n, n_total, ctypes.c_void_p(comm or 0),
+                            _ptr(coeffs), _ptr(blocks), _ptr(mean), int(bool(use_graph)), _stream_ptr(stream)),
+          "fbspca_step")
+    return blocks, mean
+
+
+def fbspca_comm_wait(comm: int, stream=None, timeout_s: float = 0.0):
+    check(lib().fbspca_comm_wait(ctypes.c_void_p(comm), _stream_ptr(stream), float(timeout_s)), "fbspca_comm_wait")
 
 
 def fbspca_nccl_unique_id() -> bytes:

@@ -233,29 +233,6 @@ def test_covariance_virtual_shards_and_partial_api():
         assert np.linalg.eigvalsh(Ck).min() >= -1e-6 * np.abs(Ck).max()
 
 
-def test_c3_full_size_sampled_parity():
-    """BASELINE configs[2] at full size in bench's launch configuration; sampled images vs the oracle."""
-    cfg = synth.config("C3")
-    n = cfg["n"]
-    imgs = synth.blob_images(cfg, 0, n, device=DEV)
-    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0)
-    coeffs = F.fbspca_expand(plan, imgs)
-    blocks, mean = F.fbspca_covariance(plan, coeffs)
-    torch.cuda.synchronize()
-    idx = [0, 1, 4095, 4096, 55_555, n - 1]
-    basis = O.build_basis(cfg["c"], cfg["R"])
-    ref = O.to_flat(O.expand(imgs[idx].double().cpu().numpy(), basis))
-    got = coeffs[:, idx].cpu().numpy().astype(np.complex128)
-    assert rel_l2_per_image(got, ref, basis).max() <= TOL32
-    # properties at full size: mean and trace bookkeeping from the GPU coefficients (S:373)
-    A0 = coeffs[: plan.p[0]].real.double()
-    assert torch.allclose(mean, A0.mean(1), rtol=1e-6, atol=1e-7)
-    tr = F.unpack_blocks(plan, blocks.cpu().numpy())
-    k = 5
-    Ak = coeffs[plan.coef_off[k]:plan.coef_off[k + 1]]
-    assert abs(np.trace(tr[k]) - (Ak.abs() ** 2).double().sum().item() / n) <= 1e-5 * np.trace(tr[k])
-
-
 def _oracle_cov_from_gpu_coeffs(coeffs, basis, chunk=8192):
     """fp64 oracle K5 (O.covariance_partials per chunk, O.finalize_covariance) on the GPU's coefficients."""
     n = coeffs.shape[1]
@@ -285,23 +262,6 @@ def _spectral_checks(plan, blocks, mean, evals, evecs, m_o, C_o, tol_c=1e-4):
     return err_c, worst
 
 
-def test_c3_full_size_spectral_parity():
-    """configs[2] at full size (100,000 images): GPU K5/K6 against the fp64 oracle K5/K6 run on the GPU's own
-    coefficients (K1-K4 are checked by sampled coefficient parity, K5-K7 this way)."""
-    cfg = synth.config("C3")
-    n = cfg["n"]
-    imgs = synth.blob_images(cfg, 0, n, device=DEV)
-    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0)
-    coeffs = F.fbspca_expand(plan, imgs)
-    del imgs
-    blocks, mean = F.fbspca_covariance(plan, coeffs)
-    evals, evecs = F.fbspca_eig(plan, blocks)
-    torch.cuda.synchronize()
-    basis = O.build_basis(cfg["c"], cfg["R"])
-    m_o, C_o = _oracle_cov_from_gpu_coeffs(coeffs, basis)
-    _spectral_checks(plan, blocks, mean, evals, evecs, m_o, C_o)
-
-
 def test_c5_full_size_sampled_expansion():
     """configs[4] at full size (50,000 images of 360 x 360) in bench.py's launch configuration (25,000-image
     expand batches): the last image of each batch (the CTAs' ragged tail) against the fp64 oracle."""
@@ -323,8 +283,8 @@ def test_c5_full_size_sampled_expansion():
 
 @pytest.mark.parametrize("name,n", [("C4", 2048), ("C5", 1024), ("RB", 2048)])
 def test_large_L_spectral_parity_subset(name, n):
-    """configs[3] (L = 256, pow2 kernels, R = 128 tensor-core covariance) and configs[4] (L = 360, runtime
-    mixed-radix FFTs, p_k up to 179): a subset of images through K1-K6, oracle K5/K6 on the GPU coefficients."""
+    """configs[3] (L = 256), configs[4] (L = 360, p_k up to 179) and the ribosome shape: a larger subset than
+    test_gpu_parity_full.py's 512 images through K1-K6, oracle K5/K6 on the GPU coefficients (checks K5-K6)."""
     cfg, imgs = blob_case(name, 0, n)
     plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=512)
     coeffs = F.fbspca_expand(plan, imgs)

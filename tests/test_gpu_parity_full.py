@@ -1,0 +1,291 @@
+"""GPU parity at the configs as BASELINE.json states them, in bench.py's launch configuration.
+
+* C2 (n = 10,000) and C3 (n = 100,000) eigenpairs and covariance blocks against CACHED fp64 oracle results for the
+  whole config (tests/golden/oracle_C{2,3}.npz, written by tools/oracle_cache.py, which calls only `synth` on the
+  CPU and `oracle/`: its own expansion, not the GPU's coefficients).  The images here are generated on the GPU by
+  the same seeded generator; a sample of them is checked against the CPU generator the cache consumed.
+* C3 coefficients of 2,048 images spread over all four 25,000-image expand batches and every CTA residue mod 148
+  (the polar kernel's persistent grid stride), plan built exactly as bench.py builds it.
+* C4 / C5: 512-image subsets, coefficients of every image and the subset's spectrum against the oracle's own
+  expansion of those images.
+* K7 (projection + MP/Wiener, modes 0/1/2) on EVERY component, both paths fed the GPU's own eigenpairs.
+* kernel instances without another test: fp32 w = 7 (eps = 1e-6, runtime-radix kernel) and fp64 with M != 64
+  (runtime radices incl. 11), and the eps contract of fbspca_plan.
+
+Bars (BASELINE.json north_star): coefficient relative l2 <= 1e-4 per image (reading Q12), top-50 eigenvalues
+within 1e-4 relative (reading Q11 pooling), principal-subspace cosine >= 0.9999 (reading Q10 near-tie extension).
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_1412_0781_b200 as F
+import synth
+
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda:0") if torch.cuda.is_available() else None
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+TOL32 = 1e-4
+BENCH_BATCH = 25000                       # bench.py BATCH: images per expand batch in the timed configuration
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as g
+    g.build()
+
+
+def rel_l2_per_image(got, ref, basis):
+    """Reading Q12: || a_gpu - a_orc || / || a_orc || per image, k > 0 rows weighted x2 (the +-k norm)."""
+    wt = np.ones(ref.shape[0])
+    wt[basis.p[0]:] = 2.0
+    num = np.sqrt((wt[:, None] * np.abs(got - ref) ** 2).sum(0))
+    den = np.sqrt((wt[:, None] * np.abs(ref) ** 2).sum(0))
+    return num / den
+
+
+def subspace_cos(Ug, Uo, lam_o, r):
+    """sigma_min(U_gpu[:, :r]^T U_orc[:, :r]), r extended across near-ties (Q10)."""
+    while r < len(lam_o) and abs(lam_o[r - 1] - lam_o[r]) <= 1e-3 * abs(lam_o[r - 1]):
+        r += 1
+    return np.linalg.svd(Ug[:, :r].T @ Uo[:, :r], compute_uv=False).min()
+
+
+def load_cache(name):
+    z = np.load(os.path.join(GOLDEN, f"oracle_{name}.npz"))
+    p = [int(x) for x in z["p"]]
+    lam, U, C, a, b = [], [], [], 0, 0
+    for pk in p:
+        lam.append(z["lam"][a:a + pk])
+        U.append(z["U"][b:b + pk * pk].reshape(pk, pk))
+        C.append(z["C"][b:b + pk * pk].reshape(pk, pk))
+        a += pk
+        b += pk * pk
+    return dict(p=p, n=int(z["n"]), mean=z["mean"], lam=lam, U=U, C=C, sha256=str(z["sha256"]),
+                sigma_n=float(z["sigma_n"]))
+
+
+def spectral_checks(plan, blocks, mean, evals, evecs, m_o, C_o, lam_o, U_o, tol_c=1e-4):
+    C_g = F.unpack_blocks(plan, blocks.cpu().numpy())
+    scale = max(np.abs(c).max() for c in C_o)
+    err_c = max(np.abs(a - b).max() for a, b in zip(C_g, C_o)) / scale
+    assert err_c <= tol_c, f"covariance blocks rel err {err_c:.2e}"
+    m_g = mean.cpu().numpy()
+    assert np.max(np.abs(m_g - m_o)) <= 1e-4 * np.abs(m_o).max(), "mean"
+    lam_g, U_g = F.split_eig(plan, evals.cpu().numpy(), evecs.cpu().numpy())
+    pool = sorted(((-l, k, i) for k, lk in enumerate(lam_o) for i, l in enumerate(lk)))[:50]
+    worst = max(abs(lam_g[k][i] - lam_o[k][i]) / abs(lam_o[k][i]) for _, k, i in pool)
+    assert worst <= 1e-4, f"top-50 eigenvalue rel err {worst:.2e}"
+    cos_min = 1.0
+    for k in sorted({k for _, k, _ in pool}):
+        r = sum(1 for _, kk, _ in pool if kk == k)
+        cos_min = min(cos_min, subspace_cos(U_g[k], U_o[k], lam_o[k], r))
+    assert cos_min >= 0.9999, f"principal-subspace cosine {cos_min:.6f}"
+    print(f"blocks rel err {err_c:.2e}, top-50 eigenvalue rel err {worst:.2e}, min subspace cosine {cos_min:.8f}")
+    return err_c, worst, cos_min
+
+
+def check_inputs_match_cpu_generator(cfg, imgs_gpu, sig, idx):
+    """The GPU-generated stack equals the CPU-generated one the cache consumed (same counter-based draws; the
+    low-pass FFT and exp/log may round differently on the two devices: at most a few fp32 ulps)."""
+    for i in idx:
+        cpu = synth.blob_images(cfg, i, 1, sigma_n=sig)[0].numpy()
+        gpu = imgs_gpu[i].cpu().numpy()
+        assert np.max(np.abs(cpu - gpu)) <= 1e-6 * np.abs(cpu).max(), f"image {i}"
+
+
+# ------------------------------------------------------------------ C2 full size vs the cached oracle
+def test_c2_full_size_spectral_vs_cached_oracle():
+    cfg = synth.config("C2")
+    cache = load_cache("C2")
+    n = cfg["n"]
+    assert cache["n"] == n
+    imgs = synth.blob_images(cfg, 0, n, device=DEV, sigma_n=cache["sigma_n"])
+    check_inputs_match_cpu_generator(cfg, imgs, cache["sigma_n"], [0, 511, 512, 4097, n - 1])
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=BENCH_BATCH)
+    coeffs = F.fbspca_expand(plan, imgs)
+    blocks, mean = F.fbspca_covariance(plan, coeffs)
+    evals, evecs = F.fbspca_eig(plan, blocks)
+    torch.cuda.synchronize()
+    spectral_checks(plan, blocks, mean, evals, evecs, cache["mean"], cache["C"], cache["lam"], cache["U"])
+
+
+# ------------------------------------------------------------------ C3 full size, bench launch configuration
+@pytest.fixture(scope="module")
+def c3_run():
+    cfg = synth.config("C3")
+    n = cfg["n"]
+    sig = synth.blobs.noise_sigma(cfg)                 # CPU, as bench.py's generator value up to rounding
+    imgs = synth.blob_images(cfg, 0, n, device=DEV, sigma_n=sig)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=BENCH_BATCH)
+    coeffs = torch.empty((plan.n_coef, n), dtype=plan.complex_dtype, device=DEV)
+    blocks = torch.empty(plan.n_blk, dtype=torch.float64, device=DEV)
+    mean = torch.empty(int(plan.p[0]), dtype=torch.float64, device=DEV)
+    F.fbspca_expand(plan, imgs, coeffs)                 # the calls bench.py's step makes, same buffers
+    F.fbspca_covariance(plan, coeffs, n, n, None, blocks, mean)
+    evals, evecs = F.fbspca_eig(plan, blocks)
+    torch.cuda.synchronize()
+    return dict(cfg=cfg, n=n, sig=sig, imgs=imgs, plan=plan, coeffs=coeffs, blocks=blocks, mean=mean,
+                evals=evals, evecs=evecs)
+
+
+def test_c3_full_size_spectral_vs_cached_oracle(c3_run):
+    cache = load_cache("C3")
+    r = c3_run
+    assert cache["n"] == r["n"] and abs(cache["sigma_n"] - r["sig"]) <= 1e-12 * r["sig"]
+    check_inputs_match_cpu_generator(r["cfg"], r["imgs"], r["sig"], [0, 24999, 25000, 77777, r["n"] - 1])
+    spectral_checks(r["plan"], r["blocks"], r["mean"], r["evals"], r["evecs"], cache["mean"], cache["C"],
+                    cache["lam"], cache["U"])
+
+
+def c3_sample_indices(n, batch, per_batch=512, seed=0):
+    """Per 25,000-image batch: the first 148 images (every CTA residue of the 148-CTA persistent grid, first pass),
+    the last 148 (every residue, ragged last pass), the batch edges, and random fill -- per_batch in total."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for b0 in range(0, n, batch):
+        b1 = min(n, b0 + batch)
+        s = set(range(b0, b0 + 148)) | set(range(b1 - 148, b1))
+        while len(s) < per_batch:
+            s.add(int(rng.integers(b0, b1)))
+        out.extend(sorted(s))
+    return np.asarray(out)
+
+
+def test_c3_sampled_coefficients_bench_config(c3_run):
+    r = c3_run
+    idx = c3_sample_indices(r["n"], BENCH_BATCH)
+    assert len(idx) == 2048 and len(set((idx % BENCH_BATCH) % 148)) == 148
+    basis = O.build_basis(r["cfg"]["c"], r["cfg"]["R"])
+    it = torch.from_numpy(idx).to(DEV)
+    ref = O.to_flat(O.expand(r["imgs"][it].double().cpu().numpy(), basis))
+    got = r["coeffs"][:, it].cpu().numpy().astype(np.complex128)
+    rel = rel_l2_per_image(got, ref, basis)
+    print(f"C3 2048 sampled images: max rel l2 {rel.max():.3e}, median {np.median(rel):.3e}")
+    assert rel.max() <= TOL32, f"max per-image rel l2 {rel.max():.3e} at image {idx[rel.argmax()]}"
+    assert np.all(got[: basis.p[0]].imag == 0)                                     # Q8
+
+
+# ------------------------------------------------------------------ C4 / C5 512-image subsets
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_large_L_512_image_subset(name):
+    cfg = synth.config(name)
+    n = 512
+    imgs = synth.blob_images(cfg, 0, n, device=DEV)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=n)
+    coeffs = F.fbspca_expand(plan, imgs)
+    blocks, mean = F.fbspca_covariance(plan, coeffs)
+    evals, evecs = F.fbspca_eig(plan, blocks)
+    torch.cuda.synchronize()
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    A = O.expand(imgs.double().cpu().numpy(), basis)
+    got = coeffs.cpu().numpy().astype(np.complex128)
+    rel = rel_l2_per_image(got, O.to_flat(A), basis)
+    print(f"{name} 512 images: max rel l2 {rel.max():.3e}")
+    assert rel.max() <= TOL32, f"{name}: max per-image rel l2 {rel.max():.3e}"
+    m_o, C_o = O.block_covariance(A)
+    lam_o, U_o = O.block_eig(C_o)
+    spectral_checks(plan, blocks, mean, evals, evecs, m_o, C_o, lam_o, U_o)
+
+
+# ------------------------------------------------------------------ K7 on every component, modes 0/1/2
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_project_every_component(mode):
+    """Eq. (sPCAcoeff) P:364 + Eq. (compselect) P:692 + P:699 (mode 2: SPEC S:442 spiked l): both paths get the
+    GPU's coefficients, mean and eigenpairs; every (k, l) row is compared."""
+    cfg = synth.config("C2")
+    n = 600
+    imgs = synth.blob_images(cfg, 0, n, device=DEV)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=256)
+    coeffs = F.fbspca_expand(plan, imgs)
+    blocks, mean = F.fbspca_covariance(plan, coeffs)
+    evals, evecs = F.fbspca_eig(plan, blocks)
+    sigma2 = float(synth.blobs.noise_sigma(cfg)) ** 2
+    out = F.fbspca_project(plan, coeffs, mean, evals, evecs, sigma2=sigma2, mode=mode)
+    torch.cuda.synchronize()
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    A = O.from_flat(coeffs.cpu().numpy().astype(np.complex128), basis)
+    lam_g, U_g = F.split_eig(plan, evals.cpu().numpy(), evecs.cpu().numpy())
+    ref = O.project(A, mean.cpu().numpy(), U_g, lam_g, basis, sigma2, mode, n)
+    got = O.from_flat(out.cpu().numpy().astype(np.complex128), basis)
+    h = O.shrink_weights(lam_g, basis, n, sigma2, mode)
+    _, Ac = O.mean_and_center(A)
+    worst = 0.0
+    for k in range(basis.k_max + 1):
+        # fp32 coefficients through a p_k-term fp32 sum: error ~ p_k u ||a_k|| per image (u = 2^-24)
+        floor = 1e-6 * np.linalg.norm(Ac[k]) / np.sqrt(n)
+        for l in range(basis.p[k]):
+            if h[k][l] == 0:
+                assert np.all(got[k][l] == 0), f"k={k} l={l}: rejected component not zero"
+                continue
+            nrm = np.linalg.norm(ref[k][l])
+            e = np.linalg.norm(got[k][l] - ref[k][l])
+            worst = max(worst, e / (nrm + 1e-300))
+            assert e <= 1e-5 * nrm + floor * np.sqrt(n), f"k={k} l={l}: {e:.3e} vs {nrm:.3e}"
+    print(f"mode {mode}: worst per-component rel err {worst:.2e}; kept {sum(int((x > 0).sum()) for x in h)} "
+          f"of {basis.n_coef}")
+
+
+def test_eigenimages_parity():
+    """NEXT-1 eigenimages: the leading eigenvectors u_l^(k) rendered as images through Eq. (IFT_FB)
+    (reading Q2) on the GPU vs the oracle's pixel synthesis of the same coefficient vectors."""
+    cfg = synth.config("C2")
+    imgs = synth.blob_images(cfg, 0, 400, device=DEV)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=256)
+    coeffs = F.fbspca_expand(plan, imgs)
+    blocks, _ = F.fbspca_covariance(plan, coeffs)
+    evals, evecs = F.fbspca_eig(plan, blocks)
+    torch.cuda.synchronize()
+    lam_g, U_g = F.split_eig(plan, evals.cpu().numpy(), evecs.cpu().numpy())
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    picks = [(0, 0), (0, 1), (1, 0), (2, 0), (5, 0), (basis.k_max, 0)]
+    flat = np.zeros((plan.n_coef, len(picks)), dtype=np.complex128)
+    for c, (k, l) in enumerate(picks):
+        flat[plan.coef_off[k]:plan.coef_off[k + 1], c] = U_g[k][:, l]
+    ct = torch.from_numpy(flat.astype(np.complex64)).to(DEV)
+    img = F.fbspca_synthesize(plan, ct)
+    torch.cuda.synchronize()
+    ref = O.synthesize_pixels(O.from_flat(flat.astype(np.complex64).astype(np.complex128), basis), basis, cfg["L"])
+    got = img.cpu().numpy().astype(np.float64)
+    for c in range(len(picks)):
+        assert np.max(np.abs(got[c] - ref[c])) <= 1e-5 * np.abs(ref[c]).max(), picks[c]
+
+
+# ------------------------------------------------------------------ kernel instances + the eps contract
+@pytest.mark.parametrize("name,n,eps", [("C2", 40, 1e-6), ("C3", 8, 1e-6), ("C2", 40, 1e-5), ("C3", 8, 1e-4)])
+def test_eps_contract_fp32(name, n, eps):
+    """fbspca_plan's eps: w = ceil(log10(1/eps)) + 1 taps (fp32: clamped to [6, 7]); eps = 1e-6 selects the w = 7
+    runtime-radix polar kernel.  Contract (include/fbspca.h): per-image coefficient rel l2 <= max(4 eps, 4e-6)."""
+    cfg = synth.config(name)
+    imgs = synth.blob_images(cfg, 0, n, device=DEV)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], eps=eps, device=0, max_batch=64)
+    assert plan.w == (7 if eps <= 1e-6 else 6)
+    got = F.fbspca_expand(plan, imgs).cpu().numpy().astype(np.complex128)
+    basis = O.build_basis(cfg["c"], cfg["R"])
+    ref = O.to_flat(O.expand(imgs.double().cpu().numpy(), basis))
+    rel = rel_l2_per_image(got, ref, basis)
+    print(f"{name} eps {eps:g} w {plan.w}: max rel l2 {rel.max():.3e}")
+    assert rel.max() <= max(4 * eps, 4e-6)
+
+
+@pytest.mark.parametrize("L,R", [(33, 16), (40, 20), (27, 13)])
+def test_expand_fp64_runtime_radix(L, R):
+    """fp64 plans with M != 64 run polar_kernel<double, 13, 0> (runtime mixed radices: M = 72, 80, 54)."""
+    rng = np.random.default_rng(L)
+    imgs = rng.standard_normal((6, L, L))
+    plan = F.fbspca_plan(L, 0.5, R, dtype=F.F64, device=0, max_batch=4)
+    assert plan.M != 64
+    got = F.fbspca_expand(plan, torch.from_numpy(imgs).to(DEV)).cpu().numpy()
+    basis = O.build_basis(0.5, R)
+    ref = O.to_flat(O.expand(imgs, basis))
+    rel = rel_l2_per_image(got, ref, basis)
+    print(f"fp64 L={L} M={plan.M}: max rel l2 {rel.max():.3e}")
+    assert rel.max() <= 1e-9

@@ -158,12 +158,14 @@ def test_direct_sum_delta_images():
     assert np.max(np.abs(F[2] - np.exp(-2j * np.pi * X2))) < 1e-14
 
 
-def test_direct_sum_matches_brute_force():
+@pytest.mark.parametrize("dense", [True, False])
+def test_direct_sum_matches_brute_force(dense):
+    """Both summation orders of O5 (dense kernel matrix / separable) against the double sum written out."""
     b = O.build_basis(0.5, 4)
     L = 9
     rng = np.random.default_rng(2)
     I = rng.standard_normal((2, L, L))
-    F = O.polar_ft_direct(I, b)
+    F = O.polar_ft_direct(I, b, dense=dense, node_chunk=7)
     xi, _, th = O.polar_grid(b)
     idx = np.arange(L) - L // 2
     for j in (0, b.n_xi - 1):
@@ -172,6 +174,15 @@ def test_direct_sum_matches_brute_force():
             ref = sum(I[1, a, bb] * np.exp(-2j * np.pi * (x1 * idx[a] + x2 * idx[bb]))
                       for a in range(L) for bb in range(L))
             assert abs(F[1, j, l] - ref) < 1e-12
+
+
+def test_direct_sum_orders_agree():
+    """The dense (n >= 32) and separable (n < 32) orders of the same sum agree to rounding at L = 33, R = 16."""
+    b = O.build_basis(0.5, 16)
+    I = np.random.default_rng(5).standard_normal((3, 33, 33))
+    Fd = O.polar_ft_direct(I, b, dense=True)
+    Fs = O.polar_ft_direct(I, b, dense=False)
+    assert np.max(np.abs(Fd - Fs)) < 1e-12 * np.abs(Fd).max()
 
 
 # ---------------------------------------------------------------- O6 angular pins (S:233-234)
