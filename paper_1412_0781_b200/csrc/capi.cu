@@ -260,6 +260,7 @@ fbspca_status upload_plan(Plan& P) {
   FB_CUDA(upload((void**)&P.d_rho, P.rho.data(), P.rho.size()), "upload rho");
   FB_CUDA(upload((void**)&P.d_cs, P.cs.data(), P.cs.size()), "upload cs");
   FB_CUDA(upload((void**)&P.d_nodes, P.nodes.data(), P.nodes.size()), "upload nodes");
+  FB_CUDA(upload((void**)&P.d_kj0, P.kj0.data(), P.kj0.size()), "upload kj0");
   FB_CUDA(upload((void**)&P.d_noderec, P.noderec.data(), P.noderec.size()), "upload node records");
   FB_CUDA(upload((void**)&P.d_dnoderec, P.dnoderec.data(), P.dnoderec.size()), "upload double node records");
   PolarParams& pp = P.pp;
@@ -285,7 +286,7 @@ fbspca_status upload_plan(Plan& P) {
   FB_CUDA(cudaMalloc((void**)&P.d_eig_sweeps, nk * sizeof(int)), "alloc eig sweeps");
   (void)ncoef;
   pp.deapod = P.d_deapod; pp.tw_M = P.d_tw_M; pp.tw_theta = P.d_tw_theta;
-  pp.rho = P.d_rho; pp.cs = P.d_cs; pp.nodes = P.d_nodes;
+  pp.rho = P.d_rho; pp.cs = P.d_cs; pp.nodes = P.d_nodes; pp.kj0 = P.d_kj0;
   pp.noderec = reinterpret_cast<const int4*>(P.d_noderec);
   pp.dnoderec = reinterpret_cast<const int4*>(P.d_dnoderec);
   pp.xscratch = P.d_xscratch; pp.pscratch = P.d_pscratch;
@@ -300,7 +301,7 @@ void free_plan(Plan& P) {
                   P.d_pscratch, P.d_ghat, P.d_partial, P.d_p, P.d_coef_off, P.d_blk_off, P.d_evec_off,
                   P.d_eig_work, P.d_eig_sweeps, P.d_coef_k, P.d_pp, P.d_cov_scratch, P.d_cov_scratch0, P.d_table_hi, P.d_table_lo, P.d_rbasis,
                   P.d_synth_rho, P.d_synth_pidx, P.d_synth_pir, P.d_synth_pcs, P.d_synth_grp,
-                  P.d_noderec, P.d_dnoderec};
+                  P.d_noderec, P.d_dnoderec, P.d_kj0};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (cudaEvent_t e : P.event_pool) cudaEventDestroy(e);
   P.event_pool.clear();

@@ -53,6 +53,7 @@ struct PolarParams {
   const double* rho;              // n_xi: xi_j * M
   const double* cs;               // half x 2: cos(theta_l), sin(theta_l)
   const uint32_t* nodes;          // (j << 16) | l, grouped by phase
+  const int* kj0;                 // per k: first ring j K4 reads (rings below carry |T_k| < 1e-9 max|T_k|; plan.cpp)
   const int4* noderec;            // per entry {b1 | b2 << 16, t1, t2, (j << 16) | l} (fp32 path)
   const int4* dnoderec;           // per double entry 2 int4 (plan.cpp "Double entries")
   void* xscratch;                 // per resident CTA: L x ncols_x complex
@@ -81,6 +82,8 @@ struct Plan {
   std::vector<double> xi, wq;
   std::vector<double> table;             // [coef row][j]: N J_k(R xi_j/c) xi_j w_j (2 pi / n_theta)
   std::vector<double> rbasis;            // [coef row][j]: N J_k(R xi_j/c)  (Eq. (sPCArad))
+  std::vector<int> kj0;                  // per k: first ring j of K4's sum (multiple of 8; 0 for fp64 plans)
+  int* d_kj0 = nullptr;
   // NUFFT
   int M = 0, w = 0;
   double beta = 0;
@@ -181,6 +184,6 @@ cudaError_t launch_radial_tma(const Plan& P, int64_t nb, int64_t i0, int64_t ld,
 cudaError_t launch_cov_tma(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb, cudaStream_t s);
 cudaError_t launch_cov_k0(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb, cudaStream_t s);
 int fft_values_per_lane(const FftPlan& f);
-int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps);
+int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps, int nk);
 
 }  // namespace fbspca

@@ -14,8 +14,8 @@ namespace fbspca {
 template <typename T>
 __global__ void __launch_bounds__(256)
 radial_kernel(const T* __restrict__ ghat, const T* __restrict__ table, const int* __restrict__ p,
-              const int64_t* __restrict__ coef_off, int nb, int n_xi, int64_t kstride, int64_t i0, int64_t ld,
-              T* __restrict__ out) {
+              const int64_t* __restrict__ coef_off, const int* __restrict__ kj0, int nb, int n_xi, int64_t kstride,
+              int64_t i0, int64_t ld, T* __restrict__ out) {
   constexpr int BM = 64, BN = 64, BK = 32;
   __shared__ T As[BK][BM + 1];
   __shared__ T Bs[BK][BN + 1];
@@ -33,7 +33,8 @@ radial_kernel(const T* __restrict__ ghat, const T* __restrict__ table, const int
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
-  for (int j0 = 0; j0 < n_xi; j0 += BK) {
+  const int jlo = kj0[k];                    // rings below carry structural zeros of T_k (plan.cpp) and no ghat
+  for (int j0 = jlo; j0 < n_xi; j0 += BK) {
     for (int e = tid; e < BM * BK; e += 256) {
       const int rr = e / BK, jj = e - rr * BK;
       const int r = r0 + rr, j = j0 + jj;
@@ -73,10 +74,10 @@ cudaError_t launch_radial(const Plan& P, int64_t nb, int64_t i0, int64_t ld, voi
   dim3 grid((unsigned)((2 * nb + 63) / 64), (unsigned)(P.k_max + 1), (unsigned)((pmax + 63) / 64));
   if (P.dt == FBSPCA_F32)
     radial_kernel<float><<<grid, 256, 0, s>>>((const float*)P.d_ghat, (const float*)P.d_table, P.d_p, P.d_coef_off,
-                                              (int)nb, P.n_xi, P.pp.ghat_kstride, i0, ld, (float*)d_coeffs);
+                                              P.d_kj0, (int)nb, P.n_xi, P.pp.ghat_kstride, i0, ld, (float*)d_coeffs);
   else
     radial_kernel<double><<<grid, 256, 0, s>>>((const double*)P.d_ghat, (const double*)P.d_table, P.d_p,
-                                               P.d_coef_off, (int)nb, P.n_xi, P.pp.ghat_kstride, i0, ld,
+                                               P.d_coef_off, P.d_kj0, (int)nb, P.n_xi, P.pp.ghat_kstride, i0, ld,
                                                (double*)d_coeffs);
   return cudaGetLastError();
 }

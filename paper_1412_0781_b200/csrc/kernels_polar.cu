@@ -97,7 +97,9 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
   T2* twM = reinterpret_cast<T2*>(base);
   T2* twT = twM + M;
   T* dap = reinterpret_cast<T*>(twT + nt);
-  T2* wscr = reinterpret_cast<T2*>(base + (((size_t)(M + nt) * sizeof(T2) + (size_t)L * sizeof(T) + 15) / 16) * 16);
+  int* skj0 = reinterpret_cast<int*>(dap + L);     // kj0[k] (K4's first ring per k) for the ghat write-out
+  T2* wscr = reinterpret_cast<T2*>(base + (((size_t)(M + nt) * sizeof(T2) + (size_t)L * sizeof(T) +
+                                            (size_t)(pp.k_max + 1) * sizeof(int) + 15) / 16) * 16);
   const int MP = (M + 15) & ~15, NTP = (nt + 15) & ~15;   // ping-pong lengths: padi permutes within 16-blocks
   T2* region = wscr + (size_t)pp.fft_warps * 2 * MP;
   // FFT groups: one warp (FG = 32) or, for M = 512 / 600 / 720 (8 ping-pong pairs fit, not 16), a warp pair (FG = 64)
@@ -120,6 +122,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       for (int i = tid; i < nt; i += nthr) twT[i] = gtT[i];
     }
     for (int i = tid; i < L; i += nthr) dap[i] = gd[i];
+    for (int i = tid; i <= pp.k_max; i += nthr) skj0[i] = pp.kj0[i];
   }
   __syncthreads();
 
@@ -533,6 +536,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           const int kk = lane >> 3, qd = lane & 7;
           T* base = ghat + img * 2 * (int64_t)n_xi + j0 + 4 * qd;
           for (int k = warp * 4 + kk; k <= kmx4; k += nwarps * 4) {
+            if (j0 + 4 * qd < skj0[k]) continue;      // below K4's first ring for k: never read (plan.cpp)
             const T2* sp = stg + (size_t)k * GS + 4 * qd;
             const T2 v0 = sp[0], v1 = sp[1], v2 = sp[2], v3 = sp[3];
             T* d = base + (int64_t)k * kstride;
@@ -555,12 +559,12 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           T2 v[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const bool ok = act && (k + u * kstep <= kmx);
+            const bool ok = act && (k + u * kstep <= kmx) && (j0 + ln >= skj0[k + u * kstep]);
             v[u] = ok ? sp[(size_t)u * kstep * GS + ln] : T2{T(0), T(0)};
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            if (act && (k + u * kstep <= kmx)) {
+            if (act && (k + u * kstep <= kmx) && (j0 + ln >= skj0[k + u * kstep])) {
               T* d = dst + (int64_t)u * kstep * kstride;
               d[ln] = v[u].x;
               d[ln + n_xi] = v[u].y;
@@ -641,8 +645,9 @@ extern "C" int fbspca_debug_phase_prof(unsigned long long* out, int n) {
 }
 #endif
 
-int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps) {
-  return (int)(((sizeof(PolarParams) + 15) / 16) * 16) + (int)((((M + n_theta) * csz + L * (csz / 2)) + 15) / 16) * 16 +
+int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps, int nk) {
+  return (int)(((sizeof(PolarParams) + 15) / 16) * 16) +
+         (int)((((M + n_theta) * csz + L * (csz / 2) + nk * (int)sizeof(int)) + 15) / 16) * 16 +
          nwarps * 2 * ((M + 15) & ~15) * csz;
 }
 

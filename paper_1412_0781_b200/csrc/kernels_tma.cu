@@ -146,6 +146,7 @@ __device__ __forceinline__ int pow2_cols(int c) { int t = 32; while (t < c) t <<
 // (x_raw T_hi, x_raw T_lo, x_lo T_hi).  Warps: 0-3 lo parts, 4 TMA, 5 MMA, 6-9 epilogue (TMEM lane quarter w % 4).
 struct K4Args {
   int k_max, n_xi, nrt, rows, nkc, stages, bmax;   // bmax = largest box b of the plan
+  const int* kj0;                                   // per k: first ring of the sum (chunks start there; plan.cpp)
   int64_t ghat_krows;                               // ghat rows per k (2 max_batch)
   int64_t i0, ld;
   const int* p;
@@ -197,14 +198,15 @@ radial_tma_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constan
         const int bi = box_idx((args.p[k] + 15) & ~15), b = 16 << bi;
         const int arow = int(k * args.ghat_krows) + rt * 128;
         const int brow = int(args.coef_off[k]);
-        for (int kc = 0; kc < args.nkc; ++kc, ++it) {
+        const int x0 = args.kj0[k], nkc = (args.n_xi - x0 + KC - 1) / KC;   // columns >= n_xi: TMA zero fill
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
           const int s = it % NS;
           bar_wait(&empty[s], ((it / NS) & 1) ^ 1);
           unsigned char* st = sm + s * stage_bytes;
           bar_expect_tx(&full[s], a_bytes + 2u * uint32_t(b) * ROWB);
-          tma_2d(st, &tm_a, kc * KC, arow, &full[s]);
-          tma_2d(st + a_bytes, &tm_bh.m[bi], kc * KC, brow, &full[s]);
-          tma_2d(st + a_bytes + b * ROWB, &tm_bl.m[bi], kc * KC, brow, &full[s]);
+          tma_2d(st, &tm_a, x0 + kc * KC, arow, &full[s]);
+          tma_2d(st + a_bytes, &tm_bh.m[bi], x0 + kc * KC, brow, &full[s]);
+          tma_2d(st + a_bytes + b * ROWB, &tm_bl.m[bi], x0 + kc * KC, brow, &full[s]);
         }
       }
     }
@@ -222,7 +224,8 @@ radial_tma_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constan
         const uint32_t d = tmem + uint32_t(a * acc_cols);
         bar_wait(&accempty[a], ((t >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        for (int kc = 0; kc < args.nkc; ++kc, ++it) {
+        const int nkc = (args.n_xi - args.kj0[k] + KC - 1) / KC;
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
           const int s = it % NS, l = it & 1;
           bar_wait(&full[s], (it / NS) & 1);
           bar_wait(&loready[l], (it >> 1) & 1);
@@ -289,8 +292,9 @@ radial_tma_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constan
   }
   // ---- warps 0-3: lo parts of every chunk into the 2-deep lo ring
   int it = 0;
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x)
-    for (int kc = 0; kc < args.nkc; ++kc, ++it) {
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int nkc = (args.n_xi - args.kj0[item / args.nrt] + KC - 1) / KC;
+    for (int kc = 0; kc < nkc; ++kc, ++it) {
       const int s = it % NS, l = it & 1;
       bar_wait(&full[s], (it / NS) & 1);
       bar_wait(&lofree[l], ((it >> 1) & 1) ^ 1);
@@ -298,6 +302,7 @@ radial_tma_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constan
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       bar_arrive(&loready[l]);
     }
+  }
   named_sync(2, 256);
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
 }
@@ -535,7 +540,7 @@ cudaError_t launch_radial_tma(const Plan& P, int64_t nb, int64_t i0, int64_t ld,
   K4Args a;
   a.k_max = P.k_max; a.n_xi = P.n_xi; a.rows = int(2 * nb); a.nrt = (a.rows + 127) / 128;
   a.nkc = (P.n_xi + KC - 1) / KC; a.bmax = bmax; a.ghat_krows = krows; a.i0 = i0; a.ld = ld;
-  a.p = P.d_p; a.coef_off = P.d_coef_off; a.out = reinterpret_cast<float*>(d_coeffs);
+  a.p = P.d_p; a.coef_off = P.d_coef_off; a.out = reinterpret_cast<float*>(d_coeffs); a.kj0 = P.d_kj0;
   const int bbox = bmax <= 16 ? 16 : bmax <= 32 ? 32 : bmax <= 64 ? 64 : bmax <= 128 ? 128 : 256;
   a.bmax = bbox;                                           // B tiles sized for the largest box
   const int stage = 128 * ROWB + 2 * bbox * ROWB;

@@ -251,6 +251,22 @@ fbspca_status build_host_plan(Plan& P) {
         P.table[row * P.n_xi + j] = b * P.xi[j] * P.wq[j] * ang;
       }
     }
+  // Structural zeros of the table: J_k(x) decays like (e x / 2k)^k below its turning point x ~ k, so for large k
+  // the inner rings (small xi_j) carry |T_k[q][j]| below 1e-9 max|T_k| -- 1/60 of an fp32 ulp of any partial sum of
+  // Eq. (a).  fp32 plans start K4's sum for block k at kj0[k], the first such j rounded down to a multiple of 8
+  // (the tf32 MMA's K step); the polar kernel does not store ghat below it.  fp64 plans sum every ring.
+  P.kj0.assign(nk, 0);
+  if (P.dt == FBSPCA_F32)
+    for (int k = 0; k < nk; ++k) {
+      double mx = 0;
+      const int64_t r0 = P.coef_off[k] * P.n_xi, r1 = P.coef_off[k + 1] * P.n_xi;
+      for (int64_t i = r0; i < r1; ++i) mx = std::max(mx, std::fabs(P.table[i]));
+      int j0 = P.n_xi;
+      for (int64_t row = P.coef_off[k]; row < P.coef_off[k + 1]; ++row)
+        for (int j = 0; j < j0; ++j)
+          if (std::fabs(P.table[row * P.n_xi + j]) > 1e-9 * mx) { j0 = j; break; }
+      P.kj0[k] = (j0 / 8) * 8;
+    }
 
   // ---- NUFFT: oversampled grid, window, deapodisation ----
   int M = 2 * L;
@@ -301,7 +317,7 @@ fbspca_status build_host_plan(Plan& P) {
   const int fft_share = (P.n_theta == 2 * M) ? 2 : 3;
   while (pp.fft_warps > 2 && pp.fft_warps * 2 * M * csz > cap / fft_share) pp.fft_warps /= 2;
   if (const char* e = getenv("FBSPCA_FFT_WARPS")) pp.fft_warps = std::max(1, std::min(16, atoi(e)));
-  const int fixed = polar_fixed_smem(M, P.n_theta, L, csz, pp.fft_warps);
+  const int fixed = polar_fixed_smem(M, P.n_theta, L, csz, pp.fft_warps, P.k_max + 1);
   const int budget = cap - fixed;
   const int kk = (P.k_max + 1) | 1;                    // staging row stride (odd)
   const int ntp = (P.n_theta + 15) & ~15;               // ping-pong length (swizzle permutes 16-blocks)
