@@ -323,6 +323,7 @@ radial_tma_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constan
 constexpr int K5_CK = 4;
 struct K5Args {
   int k_max, nchunk, chunk, drain, stages, rmax, ck;              // ck: K chunks per stage (<= K5_CK)
+  int k_lo;                                                       // first k of this launch (k_lo..k_max)
   int64_t i0, nb, ld;
   const int* p;
   const int64_t* coef_off;
@@ -361,10 +362,10 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
-  const int n_items = args.k_max * args.nchunk;
+  const int n_items = (args.k_max - args.k_lo + 1) * args.nchunk;
   const int st_per_group = max(1, (2 * args.drain) / (KC * CK));   // stages per drain group
   auto item_geom = [&](int item, int& k, int& ch, int& nkc) {
-    k = 1 + item / args.nchunk; ch = item - (k - 1) * args.nchunk;
+    k = args.k_lo + item / args.nchunk; ch = item - (k - args.k_lo) * args.nchunk;
     const int64_t img0 = args.i0 + int64_t(ch) * args.chunk;
     const int ncols = int(2 * min(int64_t(args.chunk), args.i0 + args.nb - img0));
     nkc = (ncols + KC - 1) / KC;
@@ -495,6 +496,190 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
 }
 
+
+// ---------------------------------------------------------------- K5, blocks with 128 < p_k <= 256 (C5, T3)
+// S_k in 128 x 128 output blocks (m, n) in {(0,0), (0,1), (1,1)} of the row halves x_0 = rows 0..127, x_1 = rows
+// 128..255 (rows >= p_k: the next block's rows or TMA zero fill, outputs ignored).  Item = (k, chunk, block).
+// Stage = one 32-column K chunk: [x_0; lo_0; x_1; lo_1] (512 rows; a diagonal item uses the first 256).
+//   diagonal (m = n): D = x_m [x_m; lo_m]^T (N = 256): S = X + Y + Y^T as in cov_tma_kernel;
+//   off-diagonal:     D = x_0 [x_1; lo_1]^T (N = 256) plus lo_0 x_1^T accumulated into D[:, 0:128] (N = 128):
+//                     S_01 = D[:, 0:128] + D[:, 128:256]  (= x0 x1' + lo0 x1' + x0 lo1', the 3xTF32 terms).
+// Two 256-column TMEM accumulators (double-buffered drains every `drain` images), one CTA per SM.
+__global__ void __launch_bounds__(192, 1)
+cov_tma_big_kernel(const __grid_constant__ CUtensorMap tm_a, const K5Args args) {
+  extern __shared__ __align__(1024) unsigned char sm_raw[];
+  unsigned char* sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u);
+  constexpr int RR = 128;
+  const int NS = args.stages;
+  constexpr uint32_t half_bytes = 128u * ROWB;                     // 128 rows of one K chunk
+  constexpr uint32_t stage_bytes = 4u * half_bytes;                // x_0, lo_0, x_1, lo_1
+  float* tr = reinterpret_cast<float*>(sm + NS * stage_bytes);      // 128 x 129 epilogue transpose
+  uint64_t* full = reinterpret_cast<uint64_t*>(tr + RR * (RR + 1));
+  uint64_t* loready = full + NS;
+  uint64_t* empty = loready + NS;
+  uint64_t* accfull = empty + NS;                                   // 2
+  uint64_t* accempty = accfull + 2;                                 // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int tcols = 512;                                        // two accumulators of 256 columns
+  if (warp == 0) tmem_alloc(tmem_slot, tcols);
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) { bar_init(&full[s], 1); bar_init(&loready[s], 128); bar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { bar_init(&accfull[a], 1); bar_init(&accempty[a], 128); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+  const int nk = args.k_max - args.k_lo + 1;
+  const int n_items = nk * args.nchunk * 3;
+  const int kc_per_group = max(1, (2 * args.drain) / KC);          // K chunks per drain group
+  auto item_geom = [&](int item, int& k, int& ch, int& blk, int& nkc) {
+    blk = item % 3;
+    const int r = item / 3;
+    k = args.k_lo + r / args.nchunk; ch = r - (k - args.k_lo) * args.nchunk;
+    const int64_t img0 = args.i0 + int64_t(ch) * args.chunk;
+    const int ncols = int(2 * min(int64_t(args.chunk), args.i0 + args.nb - img0));
+    nkc = (ncols + KC - 1) / KC;
+  };
+
+  if (warp == 4) {                                                  // ---- TMA producer
+    if (lane == 0) {
+      int it = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        int k, ch, blk, nkc;
+        item_geom(item, k, ch, blk, nkc);
+        const int col0 = int(2 * (args.i0 + int64_t(ch) * args.chunk));
+        const int row0 = int(args.coef_off[k]);
+        const int m = blk == 2 ? 1 : 0;
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          const int s = it % NS;
+          bar_wait(&empty[s], ((it / NS) & 1) ^ 1);
+          unsigned char* st = sm + s * stage_bytes;
+          if (blk == 1) {
+            bar_expect_tx(&full[s], 2u * half_bytes);
+            tma_2d(st, &tm_a, col0 + kc * KC, row0, &full[s]);
+            tma_2d(st + 2 * half_bytes, &tm_a, col0 + kc * KC, row0 + 128, &full[s]);
+          } else {
+            bar_expect_tx(&full[s], half_bytes);
+            tma_2d(st, &tm_a, col0 + kc * KC, row0 + 128 * m, &full[s]);
+          }
+        }
+      }
+    }
+    return;
+  }
+  if (warp == 5) {                                                  // ---- MMA issuer
+    if (lane == 0) {
+      const uint32_t id256 = idesc_tf32(128, 256), id128 = idesc_tf32(128, 128);
+      int it = 0, g = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        int k, ch, blk, nkc;
+        item_geom(item, k, ch, blk, nkc);
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          const bool first = (kc % kc_per_group) == 0;
+          const bool last = (kc % kc_per_group) == kc_per_group - 1 || kc == nkc - 1;
+          const int a = g & 1;
+          const uint32_t d = tmem + uint32_t(a * 256);
+          if (first) {
+            bar_wait(&accempty[a], ((g >> 1) & 1) ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+          }
+          const int s = it % NS;
+          bar_wait(&loready[s], (it / NS) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t x0 = su32(sm + s * stage_bytes);
+#pragma unroll
+          for (int s4 = 0; s4 < KC / 8; ++s4) {
+            const uint32_t ko = uint32_t(s4) * 32u;
+            const uint32_t acc = (!first || s4) ? 1u : 0u;
+            if (blk == 1) {
+              const uint32_t x1 = x0 + 2 * half_bytes;
+              mma_tf32(d, desc_sw128(x0 + ko), desc_sw128(x1 + ko), id256, acc);              // x0 [x1; lo1]^T
+              mma_tf32(d, desc_sw128(x0 + half_bytes + ko), desc_sw128(x1 + ko), id128, 1u);  // + lo0 x1^T
+            } else {
+              mma_tf32(d, desc_sw128(x0 + ko), desc_sw128(x0 + ko), id256, acc);              // x_m [x_m; lo_m]^T
+            }
+          }
+          mma_commit(&empty[s]);
+          if (last) { mma_commit(&accfull[a]); ++g; }
+        }
+      }
+    }
+    return;
+  }
+  // ---- warps 0-3: lo parts, drains, epilogue (thread q = row of the 128 x 128 output block)
+  const int q = 32 * warp + lane;
+  int it = 0, g = 0;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    int k, ch, blk, nkc;
+    item_geom(item, k, ch, blk, nkc);
+    const int pk = args.p[k];
+    float acc[RR];
+#pragma unroll
+    for (int i = 0; i < RR; ++i) acc[i] = 0.f;
+    auto drain = [&](int gg) {
+      const int a = gg & 1;
+      bar_wait(&accfull[a], (gg >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t tb = tmem + (uint32_t(32 * warp) << 16) + uint32_t(a * 256);
+#pragma unroll
+      for (int c1 = 0; c1 < RR; c1 += 16) {
+        uint32_t xr[16], yr[16];
+        tmem_ld16_nowait(tb + uint32_t(c1), xr);
+        tmem_ld16_nowait(tb + uint32_t(128 + c1), yr);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int c = c1 + i;
+          const float xv = __uint_as_float(xr[i]), yv = __uint_as_float(yr[i]);
+          if (blk == 1) acc[c] += xv + yv;
+          else acc[c] += c > q ? yv : c == q ? xv + 2.f * yv : xv + yv;
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      bar_arrive(&accempty[a]);
+    };
+    int pending = -1;
+    for (int kc = 0; kc < nkc; ++kc, ++it) {
+      const int s = it % NS;
+      unsigned char* st = sm + s * stage_bytes;
+      bar_wait(&full[s], (it / NS) & 1);
+      make_lo(st, st + half_bytes, half_bytes, tid);
+      if (blk == 1) make_lo(st + 2 * half_bytes, st + 3 * half_bytes, half_bytes, tid);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bar_arrive(&loready[s]);
+      const bool last = (kc % kc_per_group) == kc_per_group - 1 || kc == nkc - 1;
+      if (last) {
+        if (pending >= 0) drain(pending);
+        pending = g++;
+      }
+    }
+    drain(pending);
+    named_sync(1, 128);
+#pragma unroll
+    for (int c = 0; c < RR; ++c) tr[q * (RR + 1) + c] = acc[c];
+    named_sync(1, 128);
+    double* dst = args.scratch + int64_t(ch) * args.scratch_stride + args.blk_off[k];
+    const int m = blk == 2 ? 1 : 0, n = blk >= 1 ? 1 : 0;
+    for (int r = warp; r < 128; r += 4) {                   // packed upper-triangle rows of S_k inside the block
+      const int qr = 128 * m + r;
+      if (qr >= pk) break;
+      double* drow = dst + (int64_t)qr * pk - (int64_t)qr * (qr - 1) / 2 - qr;        // drow[col]
+      const int c0 = blk == 1 ? 0 : r;
+      for (int c = c0 + lane; c < 128 && 128 * n + c < pk; c += 32) {
+        const int qc = 128 * n + c;
+        drow[qc] = blk == 1 ? double(tr[r * (RR + 1) + c])
+                            : (c == r ? double(tr[r * (RR + 1) + r]) : double(tr[r * (RR + 1) + c]) + double(tr[c * (RR + 1) + r]));
+      }
+    }
+    named_sync(1, 128);
+  }
+  named_sync(1, 128);
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
+}
+
 // ---------------------------------------------------------------- host side
 namespace {
 
@@ -573,7 +758,7 @@ static cudaError_t launch_cov_tma_t(const Plan& P, const MapSet& ta, K5Args& a, 
   const int smem = a.stages * stage + fixed;
   cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(cov_tma_kernel<RR>), smem);
   if (e != cudaSuccess) return e;
-  const int items = a.k_max * a.nchunk;
+  const int items = (a.k_max - a.k_lo + 1) * a.nchunk;
   const int grid = std::min(items, per_sm * P.num_sms);
   cov_tma_kernel<RR><<<grid, 192, smem, s>>>(ta, a);
   return cudaGetLastError();
@@ -582,15 +767,33 @@ static cudaError_t launch_cov_tma_t(const Plan& P, const MapSet& ta, K5Args& a, 
 // k >= 1 of the batch [i0, i0 + nb) into scratch[chunk] (chunks of kCovChunk images); k = 0 is not touched.
 cudaError_t launch_cov_tma(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb, cudaStream_t s) {
   if (P.k_max < 1) return cudaSuccess;
-  const int rmax = (P.p[1] + 15) & ~15;
-  if (rmax > 128) return cudaErrorInvalidValue;             // two M tiles: not on this path
+  if (((P.p[1] + 15) & ~15) > 256) return cudaErrorInvalidValue;   // p_k > 256: not on this path
+  // k in [1, kb]: 128 < p_k <= 256 (big-block kernel); k in (kb, k_max]: p_k <= 128 (p_k is non-increasing in k)
+  int kb = 0;
+  while (kb + 1 <= P.k_max && P.p[kb + 1] > 128) ++kb;
   MapSet ta;
   for (int i = 0; i < 4; ++i)
     if (!make_map(&ta.m[i], d_coeffs, P.coef_off[P.k_max + 1], 2 * ld, 2 * ld, 16 << i)) return cudaErrorInvalidValue;
   K5Args a;
-  a.k_max = P.k_max; a.chunk = kCovChunk; a.nchunk = int((nb + kCovChunk - 1) / kCovChunk); a.drain = 128;
-  a.rmax = rmax; a.i0 = i0; a.nb = nb; a.ld = ld; a.p = P.d_p; a.coef_off = P.d_coef_off; a.blk_off = P.d_blk_off;
+  a.k_max = P.k_max; a.k_lo = kb + 1; a.chunk = kCovChunk; a.nchunk = int((nb + kCovChunk - 1) / kCovChunk);
+  a.drain = 128; a.i0 = i0; a.nb = nb; a.ld = ld; a.p = P.d_p; a.coef_off = P.d_coef_off; a.blk_off = P.d_blk_off;
   a.scratch = P.d_cov_scratch; a.scratch_stride = P.blk_off[P.k_max + 1] + P.p[0] + 1;
+  if (kb > 0) {
+    K5Args b = a;
+    b.k_lo = 1; b.k_max = kb; b.rmax = 256; b.ck = 1;
+    const int stage = 4 * 128 * ROWB;
+    const int fixed = 128 * 129 * 4 + 1024 + 256;
+    b.stages = std::max(2, std::min(4, (227 * 1024 - fixed) / stage));
+    const int smem = b.stages * stage + fixed;
+    cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(cov_tma_big_kernel), smem);
+    if (e != cudaSuccess) return e;
+    const int grid = std::min(kb * b.nchunk * 3, P.num_sms);
+    cov_tma_big_kernel<<<grid, 192, smem, s>>>(ta.m[3], b);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (kb == P.k_max) return cudaSuccess;
+  }
+  const int rmax = (P.p[kb + 1] + 15) & ~15;
+  a.rmax = rmax;
   if (rmax <= 16) return launch_cov_tma_t<16>(P, ta, a, s);
   if (rmax <= 32) return launch_cov_tma_t<32>(P, ta, a, s);
   if (rmax <= 64) return launch_cov_tma_t<64>(P, ta, a, s);

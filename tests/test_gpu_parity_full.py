@@ -289,3 +289,39 @@ def test_expand_fp64_runtime_radix(L, R):
     rel = rel_l2_per_image(got, ref, basis)
     print(f"fp64 L={L} M={plan.M}: max rel l2 {rel.max():.3e}")
     assert rel.max() <= 1e-9
+
+
+# ------------------------------------------------------------------ K5 on tcgen05 for 128 < p_k <= 256
+@pytest.mark.parametrize("name,n", [("C5", 2500), ("T3", 1100), ("C3", 2100)])
+def test_k5_partial_sums_vs_fp64(name, n):
+    """Eq. (ck) P:342 partial sums S_k = sum_i Re(a a^*) of random coefficients against fp64 numpy: C5 (p_1 = 178)
+    and T3 (p_1 = 148) run k with p_k > 128 through the big-block tcgen05 kernel (three 128 x 128 output blocks),
+    the rest through the p_k <= 128 kernel; C3 all through the latter.  3xTF32 bound: 2e-6 of the block's scale.
+    n spans two full 1024-image chunks and a ragged one."""
+    cfg = synth.config(name)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=64)
+    g = torch.Generator(device="cpu").manual_seed(7)
+    A = torch.randn((plan.n_coef, n, 2), generator=g, dtype=torch.float32)
+    scale = torch.from_numpy(np.repeat(1.0 / (1.0 + np.arange(plan.k_max + 1)) ** 0.5, plan.p)).float()
+    A = A * scale[:, None, None]
+    A[: int(plan.p[0]), :, 1] = 0                              # Im a_0 = 0 (Q8)
+    coeffs = torch.view_as_complex(A.contiguous()).to(DEV)
+    part = F.fbspca_covariance_partial(plan, coeffs)
+    torch.cuda.synchronize()
+    got = part.cpu().numpy()
+    An = coeffs.cpu().numpy().astype(np.complex128)
+    worst = 0.0
+    for k in range(plan.k_max + 1):
+        Ak = An[plan.coef_off[k]:plan.coef_off[k + 1]]
+        Sref = np.real(Ak @ np.conj(Ak).T)
+        pk = int(plan.p[k])
+        Sg = np.zeros((pk, pk))
+        Sg[np.triu_indices(pk)] = got[plan.blk_off[k]:plan.blk_off[k + 1]]
+        iu = np.triu_indices(pk)
+        err = np.abs(Sg[iu] - Sref[iu]).max() / np.abs(Sref).max()
+        worst = max(worst, err)
+        assert err <= 2e-6, f"{name} k={k} p_k={pk}: rel err {err:.2e}"
+    s0 = got[plan.blk_off[-1]:plan.blk_off[-1] + int(plan.p[0])]
+    assert np.allclose(s0, An[: int(plan.p[0])].real.sum(1), rtol=1e-9, atol=1e-6)
+    assert got[-1] == n
+    print(f"{name}: p_1 = {int(plan.p[1])}, worst block rel err {worst:.2e}")
