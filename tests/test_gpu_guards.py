@@ -30,8 +30,13 @@ def need_gpu():
 
 
 def guarded(shape, dtype):
+    """NaN-filled buffer with G guard elements on each side (complex: both parts NaN) and the output view."""
     n = int(np.prod(shape))
-    buf = torch.full((n + 2 * G,), float("nan"), dtype=dtype, device=DEV)
+    if dtype.is_complex:
+        rdt = torch.float32 if dtype == torch.complex64 else torch.float64
+        buf = torch.view_as_complex(torch.full((n + 2 * G, 2), float("nan"), dtype=rdt, device=DEV))
+    else:
+        buf = torch.full((n + 2 * G,), float("nan"), dtype=dtype, device=DEV)
     return buf, buf[G:G + n].view(*shape)
 
 
