@@ -4,6 +4,7 @@
 
 #include <algorithm>
 
+#include "fft_device.cuh"
 #include "internal.h"
 
 namespace fbspca {
@@ -535,86 +536,145 @@ cudaError_t launch_radial_eigfun(const Plan& P, const double* d_evecs, double* d
 }
 
 // ---------------------------------------------------------------- K7: Eq. (sPCAcoeff) P:364 + filter P:689-699
-template <typename T>
+// K7, Eq. (sPCAcoeff) P:364 + the filter of P:689-699 (modes: include/fbspca.h), and (BACK) the back-projection
+// a_k = U_k c_k + m of NEXT-1.  One CTA per (k, slice of images): W (= U_k, or U_k^T when BACK; fp64 -> T, row stride
+// padded to 4 for 16-B broadcast loads), the weights h_k and U_k^T m (k = 0) are staged once per CTA; thread = image,
+// its (re, im) pair accumulated together (one packed FMA per W entry) over LC outputs at a time, the input column
+// read 4 rows per batch of independent loads; the CTA strides over 256-image tiles.
+//   out[l][i] = h_l (sum_q W[q][l] in[q][i] - [k = 0] (U^T m)_l)      (project; Im = 0 at k = 0)
+//   out[q][i] = sum_l W[l][q] in[l][i] + [k = 0] m_q                  (BACK; Im = 0 at k = 0)
+template <typename T, bool BACK>
 __global__ void __launch_bounds__(256)
 project_kernel(const T* __restrict__ coeffs, int64_t n, const double* __restrict__ mean,
                const double* __restrict__ evals, const double* __restrict__ evecs, const int* __restrict__ p,
                const int64_t* __restrict__ coef_off, const int64_t* __restrict__ evec_off, double sigma2, int mode,
                int64_t n_total, T* __restrict__ out) {
-  extern __shared__ unsigned char sm_raw[];
+  using T2 = typename Cx<T>::t;
+  extern __shared__ __align__(16) unsigned char sm_raw[];
   const int k = blockIdx.y;
   const int pk = p[k];
-  T* U = reinterpret_cast<T*>(sm_raw);            // pk x pk
-  T* h = U + pk * pk;                              // pk
-  T* um = h + pk;                                  // pk: U^T mean (k = 0)
+  const int up = (pk + 3) & ~3;                    // padded row stride of W in shared memory
+  T* W = reinterpret_cast<T*>(sm_raw);             // pk x up
+  T* h = W + pk * up;                              // pk
+  T* um = h + up;                                  // pk: U^T mean (k = 0, project) or the mean (k = 0, BACK)
   const double* Uk = evecs + evec_off[k];
-  for (int i = threadIdx.x; i < pk * pk; i += blockDim.x) U[i] = T(Uk[i]);
+  for (int i = threadIdx.x; i < pk * up; i += blockDim.x) {
+    const int r = i / up, c = i - r * up;          // W[r][c] = U[r][c] (project) or U[c][r] (BACK)
+    W[i] = c < pk ? T(BACK ? Uk[c * pk + r] : Uk[r * pk + c]) : T(0);
+  }
   for (int l = threadIdx.x; l < pk; l += blockDim.x) {
-    const double lam = evals[coef_off[k] + l];
-    double hv = 1.0;
-    if (mode != 0) {
-      const double g = (k == 0) ? double(pk) / double(n_total) : double(pk) / (2.0 * double(n_total));
-      const double edge = sigma2 * (1 + sqrt(g)) * (1 + sqrt(g));
-      double ell;
-      if (mode == 1) ell = fmax(lam - sigma2, 0.0);
-      else {
-        const double t = lam - sigma2 * (1 + g);
-        ell = 0.5 * (t + sqrt(fmax(t * t - 4 * g * sigma2 * sigma2, 0.0)));
+    if constexpr (BACK) {
+      h[l] = T(1);
+      um[l] = k == 0 ? T(mean[l]) : T(0);
+    } else {
+      const double lam = evals[coef_off[k] + l];
+      double hv = 1.0;
+      if (mode != 0) {
+        const double g = (k == 0) ? double(pk) / double(n_total) : double(pk) / (2.0 * double(n_total));
+        const double edge = sigma2 * (1 + sqrt(g)) * (1 + sqrt(g));
+        double ell;
+        if (mode == 1) ell = fmax(lam - sigma2, 0.0);
+        else {
+          const double t = lam - sigma2 * (1 + g);
+          ell = 0.5 * (t + sqrt(fmax(t * t - 4 * g * sigma2 * sigma2, 0.0)));
+        }
+        hv = (lam > edge) ? (sigma2 > 0 ? ell / (ell + sigma2) : 1.0) : 0.0;
       }
-      hv = (lam > edge) ? (sigma2 > 0 ? ell / (ell + sigma2) : 1.0) : 0.0;
+      h[l] = T(hv);
+      double s = 0;
+      if (k == 0) for (int q = 0; q < pk; ++q) s += Uk[q * pk + l] * mean[q];
+      um[l] = T(s);
     }
-    h[l] = T(hv);
-    double s = 0;
-    if (k == 0) for (int q = 0; q < pk; ++q) s += Uk[q * pk + l] * mean[q];
-    um[l] = T(s);
   }
   __syncthreads();
-  const int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (col >= 2 * n) return;
-  const bool re = (col & 1) == 0;
-  const T* a = coeffs + coef_off[k] * 2 * n + col;
-  T* o = out + coef_off[k] * 2 * n + col;
-  constexpr int LC = 16;
-  for (int l0 = 0; l0 < pk; l0 += LC) {
-    T acc[LC];
+  const T2* a0 = reinterpret_cast<const T2*>(coeffs) + coef_off[k] * n;
+  T2* o0 = reinterpret_cast<T2*>(out) + coef_off[k] * n;
+  constexpr int LC = 32;
+  auto fma_row = [&](T2 (&acc)[LC], const T* wr, int l0, T2 v) {
+    if constexpr (sizeof(T) == 4) {
 #pragma unroll
-    for (int t = 0; t < LC; ++t) acc[t] = T(0);
-    for (int q = 0; q < pk; ++q) {
-      const T v = a[(int64_t)q * 2 * n];
+      for (int t = 0; t < LC; t += 4) {
+        if (l0 + t < up) {
+          const float4 w = *reinterpret_cast<const float4*>(wr + t);
+          acc[t] = rfma(w.x, v, acc[t]); acc[t + 1] = rfma(w.y, v, acc[t + 1]);
+          acc[t + 2] = rfma(w.z, v, acc[t + 2]); acc[t + 3] = rfma(w.w, v, acc[t + 3]);
+        }
+      }
+    } else {
 #pragma unroll
-      for (int t = 0; t < LC; ++t) if (l0 + t < pk) acc[t] += U[q * pk + l0 + t] * v;
+      for (int t = 0; t < LC; ++t) if (l0 + t < pk) acc[t] = rfma(wr[t], v, acc[t]);
     }
+  };
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - threadIdx.x < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i >= n) continue;
+    const T2* a = a0 + i;
+    for (int l0 = 0; l0 < pk; l0 += LC) {
+      T2 acc[LC];
 #pragma unroll
-    for (int t = 0; t < LC; ++t) {
-      const int l = l0 + t;
-      if (l < pk) {
-        T v = acc[t];
-        if (k == 0) v = re ? v - um[l] : T(0);
-        o[(int64_t)l * 2 * n] = h[l] * v;
+      for (int t = 0; t < LC; ++t) acc[t] = T2{T(0), T(0)};
+      int q = 0;
+      for (; q + 4 <= pk; q += 4) {                  // four independent loads in flight, then their FMAs
+        const T2 v0 = a[(int64_t)q * n], v1 = a[(int64_t)(q + 1) * n];
+        const T2 v2 = a[(int64_t)(q + 2) * n], v3 = a[(int64_t)(q + 3) * n];
+        fma_row(acc, W + q * up + l0, l0, v0);
+        fma_row(acc, W + (q + 1) * up + l0, l0, v1);
+        fma_row(acc, W + (q + 2) * up + l0, l0, v2);
+        fma_row(acc, W + (q + 3) * up + l0, l0, v3);
+      }
+      for (; q < pk; ++q) fma_row(acc, W + q * up + l0, l0, a[(int64_t)q * n]);
+#pragma unroll
+      for (int t = 0; t < LC; ++t) {
+        const int l = l0 + t;
+        if (l < pk) {
+          T2 v = acc[t];
+          if (BACK) { if (k == 0) v = T2{v.x + um[l], T(0)}; }
+          else {
+            if (k == 0) v = T2{v.x - um[l], T(0)};
+            v = T2{h[l] * v.x, h[l] * v.y};
+          }
+          o0[(int64_t)l * n + i] = v;
+        }
       }
     }
   }
 }
 
+template <bool BACK>
+static cudaError_t launch_transform(const Plan& P, const void* d_coeffs, int64_t n, const double* d_mean,
+                                    const double* d_evals, const double* d_evecs, double sigma2, int mode,
+                                    int64_t n_total, void* d_out, cudaStream_t s) {
+  const int pmax = P.p[0], upmax = (pmax + 3) & ~3;
+  // about 8 CTAs per SM in total over the k blocks; each strides over 256-image tiles
+  const int64_t tiles = (n + 255) / 256;
+  const int per_k = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (8LL * P.num_sms + P.k_max) / (P.k_max + 1)));
+  dim3 grid((unsigned)per_k, (unsigned)(P.k_max + 1));
+  if (P.dt == FBSPCA_F32) {
+    const int smem = (int)((size_t)(pmax * upmax + 2 * upmax) * sizeof(float));
+    cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(project_kernel<float, BACK>), smem);
+    if (e != cudaSuccess) return e;
+    project_kernel<float, BACK><<<grid, 256, smem, s>>>((const float*)d_coeffs, n, d_mean, d_evals, d_evecs, P.d_p,
+                                                        P.d_coef_off, P.d_evec_off, sigma2, mode, n_total, (float*)d_out);
+  } else {
+    const int smem = (int)((size_t)(pmax * upmax + 2 * upmax) * sizeof(double));
+    cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(project_kernel<double, BACK>), smem);
+    if (e != cudaSuccess) return e;
+    project_kernel<double, BACK><<<grid, 256, smem, s>>>((const double*)d_coeffs, n, d_mean, d_evals, d_evecs, P.d_p,
+                                                         P.d_coef_off, P.d_evec_off, sigma2, mode, n_total,
+                                                         (double*)d_out);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_project(const Plan& P, const void* d_coeffs, int64_t n, const double* d_mean,
                            const double* d_evals, const double* d_evecs, double sigma2, int mode, int64_t n_total,
                            void* d_out, cudaStream_t s) {
-  const int pmax = P.p[0];
-  dim3 grid((unsigned)((2 * n + 255) / 256), (unsigned)(P.k_max + 1));
-  if (P.dt == FBSPCA_F32) {
-    const size_t smem = (size_t)(pmax * pmax + 2 * pmax) * sizeof(float);
-    cudaError_t e = cudaFuncSetAttribute(project_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    project_kernel<float><<<grid, 256, smem, s>>>((const float*)d_coeffs, n, d_mean, d_evals, d_evecs, P.d_p,
-                                                  P.d_coef_off, P.d_evec_off, sigma2, mode, n_total, (float*)d_out);
-  } else {
-    const size_t smem = (size_t)(pmax * pmax + 2 * pmax) * sizeof(double);
-    cudaError_t e = cudaFuncSetAttribute(project_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    project_kernel<double><<<grid, 256, smem, s>>>((const double*)d_coeffs, n, d_mean, d_evals, d_evecs, P.d_p,
-                                                   P.d_coef_off, P.d_evec_off, sigma2, mode, n_total, (double*)d_out);
-  }
-  return cudaGetLastError();
+  return launch_transform<false>(P, d_coeffs, n, d_mean, d_evals, d_evecs, sigma2, mode, n_total, d_out, s);
+}
+
+cudaError_t launch_backproject(const Plan& P, const void* d_c, int64_t n, const double* d_mean, const double* d_evecs,
+                               void* d_out, cudaStream_t s) {
+  return launch_transform<true>(P, d_c, n, d_mean, nullptr, d_evecs, 0.0, 0, n, d_out, s);
 }
 
 }  // namespace fbspca

@@ -69,26 +69,7 @@ synth_kernel(const T* __restrict__ coeffs, int64_t ld, const int* __restrict__ p
   for (int t = threadIdx.x; t < np; t += blockDim.x) o[pix_idx[p0 + t]] = T(acc[t]);
 }
 
-// a_k = U_k c_k (+ mean at k = 0), one thread per (image column, k) row block
-template <typename T>
-__global__ void __launch_bounds__(256)
-backproject_kernel(const T* __restrict__ c, int64_t n, const double* __restrict__ mean, const double* __restrict__ evecs,
-                   const int* __restrict__ p, const int64_t* __restrict__ coef_off, const int64_t* __restrict__ evec_off,
-                   T* __restrict__ out) {
-  const int k = blockIdx.y, pk = p[k];
-  const int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;     // re/im interleaved column
-  if (col >= 2 * n) return;
-  const double* Uk = evecs + evec_off[k];
-  const T* ck = c + coef_off[k] * 2 * n + col;
-  T* ok = out + coef_off[k] * 2 * n + col;
-  const bool re = (col & 1) == 0;
-  for (int q = 0; q < pk; ++q) {
-    double s = 0.0;
-    for (int l = 0; l < pk; ++l) s = fma(__ldg(Uk + q * pk + l), double(ck[(int64_t)l * 2 * n]), s);
-    if (k == 0) s = re ? s + mean[q] : 0.0;
-    ok[(int64_t)q * 2 * n] = T(s);
-  }
-}
+// a_k = U_k c_k (+ mean at k = 0): launch_backproject in kernels_linalg.cu (shares the K7 kernel)
 
 // ---------------------------------------------------------------- host
 static void build_synth_tables(Plan& P, std::vector<int>& pidx, std::vector<int>& pir, std::vector<double>& pcs,
@@ -181,18 +162,6 @@ cudaError_t launch_synthesize(Plan& P, const void* d_coeffs, int64_t n, void* d_
                                                  reinterpret_cast<const double2*>(P.d_synth_pcs), P.d_synth_grp, elems,
                                                  (double*)d_images);
   }
-  return cudaGetLastError();
-}
-
-cudaError_t launch_backproject(const Plan& P, const void* d_c, int64_t n, const double* d_mean, const double* d_evecs,
-                               void* d_out, cudaStream_t s) {
-  dim3 grid((unsigned)((2 * n + 255) / 256), (unsigned)(P.k_max + 1));
-  if (P.dt == FBSPCA_F32)
-    backproject_kernel<float><<<grid, 256, 0, s>>>((const float*)d_c, n, d_mean, d_evecs, P.d_p, P.d_coef_off,
-                                                   P.d_evec_off, (float*)d_out);
-  else
-    backproject_kernel<double><<<grid, 256, 0, s>>>((const double*)d_c, n, d_mean, d_evecs, P.d_p, P.d_coef_off,
-                                                    P.d_evec_off, (double*)d_out);
   return cudaGetLastError();
 }
 
