@@ -35,6 +35,7 @@ struct PolarParams {
   int phase_lo[kMaxPhases];       // first column (m2) of phase p
   int phase_node_begin[kMaxPhases + 1];
   int phase_dbl_begin[kMaxPhases + 1];       // double entries (2 int4 each) of phase p: [begin[p], begin[p+1])
+  int phase_quad_begin[kMaxPhases + 1];      // quad entries (3 int4 each) of phase p
   double beta;
   double half_w;                  // w/2
   int nwarps;                     // warps per CTA (gather, fills)
@@ -56,6 +57,7 @@ struct PolarParams {
   const int* kj0;                 // per k: first ring j K4 reads (rings below carry |T_k| < 1e-9 max|T_k|; plan.cpp)
   const int4* noderec;            // per entry {b1 | b2 << 16, t1, t2, (j << 16) | l} (fp32 path)
   const int4* dnoderec;           // per double entry 2 int4 (plan.cpp "Double entries")
+  const int4* qnoderec;           // per quad entry 3 int4 (plan.cpp "Quad entries")
   void* xscratch;                 // per resident CTA: L x ncols_x complex
   void* pscratch;                 // per resident CTA: n_xi x half complex
   int64_t ghat_kstride;           // ghat elements (T) per k: 2 max_batch n_xi (fixed, so one TMA map serves all batches)
@@ -93,6 +95,8 @@ struct Plan {
   std::vector<uint32_t> nodes;
   std::vector<int32_t> noderec;          // 4 per node entry
   std::vector<int32_t> dnoderec;         // 8 per double entry
+  std::vector<int32_t> qnoderec;         // 12 per quad entry
+  int32_t* d_qnoderec = nullptr;
   int polar_smem = 0;
   int polar_grid = 0;                    // resident CTAs of the polar kernel
   // device buffers

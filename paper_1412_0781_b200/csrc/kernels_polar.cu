@@ -244,6 +244,64 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       __syncthreads();
       PROF_MARK(2);
       if constexpr (sizeof(T) == 4 && W == 6 && MC > 0) {
+        // quad entries: leaders a = (j, l), b = (j, l + 1), c = (j + 1, l), d = (j + 1, l + 1) over one shared 7 x 7
+        // window at U, first the four direct nodes (rows U1 + r), then their four mirrors (rows -U1 - r): 49 grid
+        // loads per four nodes (plan.cpp "Quad entries")
+        {
+          const int qb = pp.phase_quad_begin[ph], qe = pp.phase_quad_begin[ph + 1];
+          for (int t = qb + tid; t < qe; t += nthr) {
+            const int4 r0 = __ldg(pp.qnoderec + 3 * t), r1 = __ldg(pp.qnoderec + 3 * t + 1), r2 = __ldg(pp.qnoderec + 3 * t + 2);
+            const int u1 = int(short(r0.x & 0xFFFF)), u2 = r0.x >> 16, of = r0.y;
+            const int jq = int(uint32_t(r0.z) >> 16), lq = r0.z & 0xFFFF;
+            const float tq[8] = {__int_as_float(r1.x), __int_as_float(r1.y), __int_as_float(r1.z), __int_as_float(r1.w),
+                                 __int_as_float(r2.x), __int_as_float(r2.y), __int_as_float(r2.z), __int_as_float(r2.w)};
+            float xq[4][7], yq[4][7];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float wq[6], vq[6];
+#pragma unroll
+              for (int q = 0; q < 6; ++q) { wq[q] = phi(tq[2 * i] - float(q)); vq[q] = phi(tq[2 * i + 1] - float(q)); }
+              const bool o1 = (of >> (2 * i)) & 1, o2 = (of >> (2 * i + 1)) & 1;
+#pragma unroll
+              for (int r = 0; r < 7; ++r) {
+                xq[i][r] = o1 ? (r ? wq[r - 1] : 0.f) : (r < 6 ? wq[r] : 0.f);
+                yq[i][r] = o2 ? (r ? vq[r - 1] : 0.f) : (r < 6 ? vq[r] : 0.f);
+              }
+            }
+            const T2* gcol = Gc + (u2 - lo);
+#pragma unroll 1
+            for (int mir = 0; mir < 2; ++mir) {
+              T2 acc[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) acc[i] = T2{0.f, 0.f};
+#pragma unroll
+              for (int r = 0; r < 7; ++r) {
+                const T2* gr = gcol + (size_t)(mir ? row0 - u1 - r : u1 + r + row0) * S;
+                T2 g[7];
+#pragma unroll
+                for (int c = 0; c < 7; ++c) g[c] = gr[c];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  T2 sacc = T2{0.f, 0.f};
+#pragma unroll
+                  for (int c = 0; c < 7; ++c) sacc = rfma(yq[i][c], g[c], sacc);
+                  acc[i] = rfma(xq[i][r], sacc, acc[i]);
+                }
+              }
+              if (!mir) {
+                Pol[(int64_t)jq * half + lq] = acc[0];
+                Pol[(int64_t)jq * half + lq + 1] = acc[1];
+                Pol[(int64_t)(jq + 1) * half + lq] = acc[2];
+                Pol[(int64_t)(jq + 1) * half + lq + 1] = acc[3];
+              } else {
+                Pol[(int64_t)jq * half + (half - lq)] = acc[0];
+                Pol[(int64_t)jq * half + (half - lq - 1)] = acc[1];
+                Pol[(int64_t)(jq + 1) * half + (half - lq)] = acc[2];
+                Pol[(int64_t)(jq + 1) * half + (half - lq - 1)] = acc[3];
+              }
+            }
+          }
+        }
         // double entries: nodes a, b of one ring (+ their mirrors) over one shared 7 x 7 window at U
         const int db = pp.phase_dbl_begin[ph], de = pp.phase_dbl_begin[ph + 1];
         // records are loaded one iteration ahead (an L2 round trip per entry was the loop's top stall)
@@ -359,7 +417,11 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
     // (the real-input pair trick on each parity; w^l shifts the odd frequencies onto the N-point grid).
     // Runtime sizes: one full n_theta-point FFT per ring rebuilt from the half ring.
     T2* stg = (MC > 0 || pp.ring_pairs) ? region : region + (size_t)pp.ang_warps * 2 * NTP;
-    const int GS = G | 1;                            // odd staging stride (bank spread)
+    const int GS = (G + 1) | 1;                      // odd staging stride >= G + 1 (bank spread, spare slot)
+    // staging index of (k, ring jj): row k at k GS, shifted by one slot for k mod 32 >= 16, so that the writers' even
+    // (or odd) k of a half-warp (k = 2m, m = 0..15) and the write-out's four consecutive k of a half-warp land in
+    // distinct 8-byte bank pairs (no 2-way conflicts; GS odd, <= 33 rings per row + 1 spare slot)
+    auto sidx = [GS](int k, int jj) { return (size_t)k * GS + jj + ((k >> 4) & 1); };
     // MC = 256 (one ring pair per warp per group): the pair's first-stage inputs f[lane + 32 r], r < 8, of both
     // rings are loaded into registers one group ahead (the loads of group j0 + G fly during group j0's FFTs and
     // write-out), and feed both the U and the V transform -- one L2 read of the polar samples, latency hidden.
@@ -411,8 +473,8 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             T2 uc = res[padi(m == 0 ? 0 : MC - m)];
             uc.y = -uc.y;
             const T2 sp = cadd(u, uc), dm = csub(u, uc);
-            stg[(size_t)(2 * m) * GS + jj] = sp;
-            if (two) stg[(size_t)(2 * m) * GS + jj + 1] = T2{dm.y, -dm.x};
+            stg[sidx(2 * m, jj)] = sp;
+            if (two) stg[sidx(2 * m, jj + 1)] = T2{dm.y, -dm.x};
           }
           __syncwarp();
           PROF_MARK(6);
@@ -427,8 +489,8 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             T2 vc = res[padi(MC - 1 - m)];
             vc.y = -vc.y;
             const T2 sp = cadd(v, vc), dm = csub(v, vc);
-            stg[(size_t)(2 * m + 1) * GS + jj] = T2{-sp.y, sp.x};
-            if (two) stg[(size_t)(2 * m + 1) * GS + jj + 1] = dm;
+            stg[sidx(2 * m + 1, jj)] = T2{-sp.y, sp.x};
+            if (two) stg[sidx(2 * m + 1, jj + 1)] = dm;
           }
           __syncwarp();
           PROF_MARK(7);
@@ -452,8 +514,8 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             T2 uc = res[padi(m == 0 ? 0 : MC - m)];
             uc.y = -uc.y;
             const T2 sp = cadd(u, uc), dm = csub(u, uc);
-            stg[(size_t)(2 * m) * GS + jj] = sp;
-            if (two) stg[(size_t)(2 * m) * GS + jj + 1] = T2{dm.y, -dm.x};
+            stg[sidx(2 * m, jj)] = sp;
+            if (two) stg[sidx(2 * m, jj + 1)] = T2{dm.y, -dm.x};
           }
           gsync<FG>(gbar);
           auto ldv = [&](int t) -> T2 {
@@ -467,8 +529,8 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             T2 vc = res[padi(MC - 1 - m)];
             vc.y = -vc.y;
             const T2 sp = cadd(v, vc), dm = csub(v, vc);
-            stg[(size_t)(2 * m + 1) * GS + jj] = T2{-sp.y, sp.x};
-            if (two) stg[(size_t)(2 * m + 1) * GS + jj + 1] = dm;
+            stg[sidx(2 * m + 1, jj)] = T2{-sp.y, sp.x};
+            if (two) stg[sidx(2 * m + 1, jj + 1)] = dm;
           }
           gsync<FG>(gbar);
         }
@@ -490,8 +552,8 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             T2 uc = res[padi(m == 0 ? 0 : Mr - m)];
             uc.y = -uc.y;
             const T2 sp = cadd(u, uc), dm = csub(u, uc);
-            stg[(size_t)(2 * m) * GS + jj] = sp;
-            if (two) stg[(size_t)(2 * m) * GS + jj + 1] = T2{dm.y, -dm.x};
+            stg[sidx(2 * m, jj)] = sp;
+            if (two) stg[sidx(2 * m, jj + 1)] = T2{dm.y, -dm.x};
           }
           __syncwarp();
           auto ldv = [&](int t) -> T2 {
@@ -505,8 +567,8 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             T2 vc = res[padi(Mr - 1 - m)];
             vc.y = -vc.y;
             const T2 sp = cadd(v, vc), dm = csub(v, vc);
-            stg[(size_t)(2 * m + 1) * GS + jj] = T2{-sp.y, sp.x};
-            if (two) stg[(size_t)(2 * m + 1) * GS + jj + 1] = dm;
+            stg[sidx(2 * m + 1, jj)] = T2{-sp.y, sp.x};
+            if (two) stg[sidx(2 * m + 1, jj + 1)] = dm;
           }
           __syncwarp();
         }
@@ -519,7 +581,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             return T2{v.x, -v.y};
           };
           const int kmx = pp.k_max;
-          auto st = [&](int t, T2 v) { if (t <= kmx) stg[(size_t)t * GS + jj] = v; };
+          auto st = [&](int t, T2 v) { if (t <= kmx) stg[sidx(t, jj)] = v; };
           if constexpr (NC > 0) fft_ct<T2, NC>(ld, st, angA, angB, twT, lane);
           else fft_rt<T2, sizeof(T) == 4>(pp.fft_theta, ld, st, angA, angB, twT, lane);
         }
@@ -532,16 +594,20 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         const int64_t kstride = pp.ghat_kstride;
         const int kmx4 = pp.k_max;
         if (sizeof(T) == 4 && g == 32 && (n_xi & 3) == 0) {
-          // full fp32 group: lane = (k of 4, quad of 4 rings); 16-byte stores of the re and im rows
-          const int kk = lane >> 3, qd = lane & 7;
-          T* base = ghat + img * 2 * (int64_t)n_xi + j0 + 4 * qd;
-          for (int k = warp * 4 + kk; k <= kmx4; k += nwarps * 4) {
-            if (j0 + 4 * qd < skj0[k]) continue;      // below K4's first ring for k: never read (plan.cpp)
-            const T2* sp = stg + (size_t)k * GS + 4 * qd;
-            const T2 v0 = sp[0], v1 = sp[1], v2 = sp[2], v3 = sp[3];
-            T* d = base + (int64_t)k * kstride;
-            __stcs(reinterpret_cast<float4*>(d), make_float4(v0.x, v1.x, v2.x, v3.x));        // streamed: read
-            __stcs(reinterpret_cast<float4*>(d + n_xi), make_float4(v0.y, v1.y, v2.y, v3.y)); // back by K4 only
+          // full fp32 group: lane = (k of 8, quad of 4 rings) over two halves of 16 rings; 16-byte stores of the re
+          // and im rows.  A half-warp reads 4 consecutive k x 4 quads: distinct bank pairs under sidx.
+          const int kk = lane >> 2, qd = lane & 3;
+          for (int hh = 0; hh < 2; ++hh) {
+            const int jr = 16 * hh + 4 * qd;
+            T* base = ghat + img * 2 * (int64_t)n_xi + j0 + jr;
+            for (int k = warp * 8 + kk; k <= kmx4; k += nwarps * 8) {
+              if (j0 + jr < skj0[k]) continue;        // below K4's first ring for k: never read (plan.cpp)
+              const T2* sp = stg + sidx(k, jr);
+              const T2 v0 = sp[0], v1 = sp[1], v2 = sp[2], v3 = sp[3];
+              T* d = base + (int64_t)k * kstride;
+              __stcs(reinterpret_cast<float4*>(d), make_float4(v0.x, v1.x, v2.x, v3.x));        // streamed: read
+              __stcs(reinterpret_cast<float4*>(d + n_xi), make_float4(v0.y, v1.y, v2.y, v3.y)); // back by K4 only
+            }
           }
         } else {
         // warp per k: lanes write rings j0 + lane (re row then im row), 128-B coalesced stores
@@ -550,7 +616,6 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         const int sub = per == 2 ? (lane >> 4) : 0, ln = per == 2 ? (lane & 15) : lane, lstep = per == 2 ? 16 : 32;
         const int k0 = warp * per + sub, kstep = nwarps * per;
         T* dst = ghat + img * 2 * (int64_t)n_xi + j0 + (int64_t)k0 * kstride;
-        const T2* sp = stg + (size_t)k0 * GS;
         const int kmx = pp.k_max;
         (void)lstep;                                  // g <= G <= 32: one element per lane and k
         const bool act = ln < g;
@@ -560,7 +625,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const bool ok = act && (k + u * kstep <= kmx) && (j0 + ln >= skj0[k + u * kstep]);
-            v[u] = ok ? sp[(size_t)u * kstep * GS + ln] : T2{T(0), T(0)};
+            v[u] = ok ? stg[sidx(k + u * kstep, ln)] : T2{T(0), T(0)};
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -571,7 +636,6 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             }
           }
           dst += 4 * (int64_t)kstep * kstride;
-          sp += (size_t)4 * kstep * GS;
         }
         }
       }

@@ -327,7 +327,7 @@ fbspca_status build_host_plan(Plan& P) {
   int Gsel = 1;
   for (auto& c : cand) {
     const int g = std::min(c[1], P.n_xi);
-    if (c[0] * 2 * ntp * csz + (g | 1) * kk * csz <= budget) { pp.ang_warps = c[0]; Gsel = g; break; }
+    if (c[0] * 2 * ntp * csz + ((g + 1) | 1) * kk * csz <= budget) { pp.ang_warps = c[0]; Gsel = g; break; }
   }
   if (pp.ang_warps < 1 || budget < M * 11 * csz) {
     set_error("image too large for the fused polar kernel's shared memory"); return FBSPCA_ERR_CONFIG;
@@ -345,19 +345,19 @@ fbspca_status build_host_plan(Plan& P) {
   pp.ring_pairs = ring_pairs ? 1 : 0;
   if (ring_pairs) {
     Gsel = std::min(32, P.n_xi);
-    while (Gsel > 2 && (Gsel | 1) * kk * csz > std::max(rows_g * S * csz, pp.fft_warps * M * csz)) Gsel /= 2;
+    while (Gsel > 2 && ((Gsel + 1) | 1) * kk * csz > std::max(rows_g * S * csz, pp.fft_warps * M * csz)) Gsel /= 2;
   }
   const int G = Gsel;
   pp.ring_group = G;
   const int region = std::max(std::max(rows_g * S * csz, pp.fft_warps * M * csz),
-                              (ring_pairs ? 0 : ang_scr) + (G | 1) * kk * csz);
+                              (ring_pairs ? 0 : ang_scr) + ((G + 1) | 1) * kk * csz);
   pp.smem_region_bytes = region;
   {   // image staged behind the phase-0 grid rows (pow2) or the per-warp row results (runtime sizes)
     const int used = std::max(L * S, pp.fft_warps * M);            // complex elements
     const int need = used + (L * L * (csz / 2) + csz - 1) / csz + 2;
     pp.img_off = (need * csz <= region) ? ((used + 1) & ~1) : -1;    // 16-B aligned start
     // the angular pass uses the region below img_off only (staging [k][ring], + ping-pongs on runtime sizes)
-    const int ang_use = (ring_pairs ? 0 : ang_scr) + (G | 1) * kk * csz;
+    const int ang_use = (ring_pairs ? 0 : ang_scr) + ((G + 1) | 1) * kk * csz;
     pp.img_prefetch = (pp.img_off >= 0 && ang_use <= pp.img_off * csz) ? 1 : 0;
   }
   P.polar_smem = fixed + region;
@@ -381,13 +381,41 @@ fbspca_status build_host_plan(Plan& P) {
     return (u2 + w <= last) ? p : -1;
   };
   const bool doubles = P.dt == FBSPCA_F32 && w == 6 && pow2_kernel && !getenv("FBSPCA_NO_DOUBLES");
-  std::vector<std::vector<std::array<int, 3>>> ph_single(phase_lo.size()), ph_double(phase_lo.size());
+  std::vector<std::vector<std::array<int, 3>>> ph_single(phase_lo.size()), ph_double(phase_lo.size()),
+      ph_quad(phase_lo.size());
   std::vector<uint32_t> singles;
   std::vector<std::array<uint32_t, 2>> dbl;
+  // Quad entries (same kernels): pair leaders (j, l), (j, l + 1), (j + 1, l), (j + 1, l + 1) of two adjacent rings
+  // whose four anchors differ by at most 1 in each direction share one (w + 1) x (w + 1) window: 49 grid loads for
+  // the four direct nodes and 49 for their four mirrors -- half the loads per node of a double entry.  Formed
+  // greedily over ring pairs (j even) before the doubles; their leaders are skipped below.
+  std::vector<std::array<uint32_t, 1>> quad;                 // (j << 16) | l of the first leader
+  std::vector<char> in_quad(size_t(P.n_xi) * (half + 1), 0);
+  // measured on B200 (C3): quads cut the gather's shared wavefronts 12 % but ran 2-4 % slower (more registers: spills in
+  // the ring pass, more bank conflicts among the fewer doubles) -- kept behind FBSPCA_QUADS=1 for experiments
+  const bool quads = doubles && getenv("FBSPCA_QUADS") && atoi(getenv("FBSPCA_QUADS")) == 1;
+  if (quads)
+    for (int j = 0; j + 1 < P.n_xi; j += 2)
+      for (int l = 1; 2 * (l + 1) < half;) {
+        const auto a = anchor(j, l), b = anchor(j, l + 1), c2 = anchor(j + 1, l), d = anchor(j + 1, l + 1);
+        const int lo1 = std::min({a.first, b.first, c2.first, d.first}), hi1 = std::max({a.first, b.first, c2.first, d.first});
+        const int lo2 = std::min({a.second, b.second, c2.second, d.second}), hi2 = std::max({a.second, b.second, c2.second, d.second});
+        const int p = phase_of_double(lo2);
+        if (hi1 - lo1 <= 1 && hi2 - lo2 <= 1 && p >= 0) {
+          ph_quad[p].push_back({lo1, lo2, int(quad.size())});
+          quad.push_back({(uint32_t(j) << 16) | uint32_t(l)});
+          for (int dj = 0; dj < 2; ++dj)
+            for (int dl = 0; dl < 2; ++dl) in_quad[size_t(j + dj) * (half + 1) + l + dl] = 1;
+          l += 2;
+        } else {
+          ++l;
+        }
+      }
   for (int j = 0; j < P.n_xi; ++j) {
     for (int l = 0; 2 * l <= half; ++l) {
+      if (in_quad[size_t(j) * (half + 1) + l]) continue;
       const auto a = anchor(j, l);
-      if (doubles && l >= 1 && 2 * (l + 1) < half) {
+      if (doubles && l >= 1 && 2 * (l + 1) < half && !in_quad[size_t(j) * (half + 1) + l + 1]) {
         const auto b = anchor(j, l + 1);
         const int u1 = std::min(a.first, b.first), u2 = std::min(a.second, b.second);
         const int p = phase_of_double(u2);
@@ -404,11 +432,35 @@ fbspca_status build_host_plan(Plan& P) {
   }
   P.nodes.clear();
   P.dnoderec.clear();
+  P.qnoderec.clear();
   int np = 0;
   for (size_t p = 0; p < phase_lo.size(); ++p) {
     pp.phase_lo[np] = phase_lo[p];
     pp.phase_node_begin[np] = int(P.nodes.size());
     pp.phase_dbl_begin[np] = int(P.dnoderec.size() / 8);
+    pp.phase_quad_begin[np] = int(P.qnoderec.size() / 12);
+    for (uint32_t id : pack_gather_items(ph_quad[p], S)) {
+      // {U1 | U2 << 16, offsets (2 bits per node: o1 | o2 << 1), (j << 16) | l, 0}, {t1, t2} of nodes a, b, c, d
+      // (a = (j, l), b = (j, l + 1), c = (j + 1, l), d = (j + 1, l + 1)); t = k - b of each node's own anchor
+      const uint32_t nd = quad[id][0];
+      const int j = int(nd >> 16), l = int(nd & 0xffffu);
+      const int jj[4] = {j, j, j + 1, j + 1}, ll[4] = {l, l + 1, l, l + 1};
+      std::pair<int, int> an[4];
+      int u1 = 1 << 30, u2 = 1 << 30;
+      for (int i = 0; i < 4; ++i) { an[i] = anchor(jj[i], ll[i]); u1 = std::min(u1, an[i].first); u2 = std::min(u2, an[i].second); }
+      int32_t rec[12] = {0};
+      rec[0] = int32_t((uint32_t(u1) & 0xFFFFu) | (uint32_t(u2) << 16));
+      int of = 0;
+      for (int i = 0; i < 4; ++i) {
+        of |= ((an[i].first - u1) | ((an[i].second - u2) << 1)) << (2 * i);
+        const float t1 = float(rho[jj[i]] * cs[2 * ll[i]] - an[i].first), t2 = float(rho[jj[i]] * cs[2 * ll[i] + 1] - an[i].second);
+        std::memcpy(&rec[4 + 2 * i], &t1, 4);
+        std::memcpy(&rec[5 + 2 * i], &t2, 4);
+      }
+      rec[1] = of;
+      rec[2] = int32_t(nd);
+      P.qnoderec.insert(P.qnoderec.end(), rec, rec + 12);
+    }
     for (uint32_t id : pack_gather_items(ph_single[p], S)) P.nodes.push_back(singles[id]);
     for (uint32_t id : pack_gather_items(ph_double[p], S)) {
       // {U1 | U2 << 16, t1a, t2a, offsets}, {node a, t1b, t2b, node b}; t = k - b of each node's own anchor
@@ -428,13 +480,14 @@ fbspca_status build_host_plan(Plan& P) {
       P.dnoderec.insert(P.dnoderec.end(), rec, rec + 8);
     }
     if (getenv("FBSPCA_DEBUG_PLAN"))
-      fprintf(stderr, "phase %d: lo %d, %zu single pair-leaders, %zu doubles\n", np, phase_lo[p], ph_single[p].size(),
-              ph_double[p].size());
+      fprintf(stderr, "phase %d: lo %d, %zu single pair-leaders, %zu doubles, %zu quads\n", np, phase_lo[p],
+              ph_single[p].size(), ph_double[p].size(), ph_quad[p].size());
     ++np;
   }
   pp.n_phase = np;
   pp.phase_node_begin[np] = int(P.nodes.size());
   pp.phase_dbl_begin[np] = int(P.dnoderec.size() / 8);
+  pp.phase_quad_begin[np] = int(P.qnoderec.size() / 12);
   P.rho = rho;
   P.cs = cs;
   // per-entry record for the fp32 gather: {b1 | b2 << 16, t1, t2, (j << 16) | l}, the same fp64 arithmetic
