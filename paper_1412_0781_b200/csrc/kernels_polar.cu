@@ -244,6 +244,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       __syncthreads();
       PROF_MARK(2);
       if constexpr (sizeof(T) == 4 && W == 6 && MC > 0) {
+#ifdef FBSPCA_QUAD_GATHER   // measured slower on B200; the plan emits quads only with FBSPCA_QUADS=1
         // quad entries: leaders a = (j, l), b = (j, l + 1), c = (j + 1, l), d = (j + 1, l + 1) over one shared 7 x 7
         // window at U, first the four direct nodes (rows U1 + r), then their four mirrors (rows -U1 - r): 49 grid
         // loads per four nodes (plan.cpp "Quad entries")
@@ -302,6 +303,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             }
           }
         }
+#endif
         // double entries: nodes a, b of one ring (+ their mirrors) over one shared 7 x 7 window at U
         const int db = pp.phase_dbl_begin[ph], de = pp.phase_dbl_begin[ph + 1];
         // records are loaded one iteration ahead (an L2 round trip per entry was the loop's top stall)
@@ -350,11 +352,19 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             aa = rfma(xa[r], sa, aa); ab = rfma(xb[r], sb, ab);
             ma = rfma(xa[r], na, ma); mb = rfma(xb[r], nb2, mb);
           }
-          const int ja = int(uint32_t(r1.x) >> 16), la = r1.x & 0xFFFF, jb = int(uint32_t(r1.w) >> 16), lb = r1.w & 0xFFFF;
-          Pol[(int64_t)ja * half + la] = aa;
-          Pol[(int64_t)ja * half + (half - la)] = ma;
-          Pol[(int64_t)jb * half + lb] = ab;
-          Pol[(int64_t)jb * half + (half - lb)] = mb;
+          const int ja = int(uint32_t(r1.x) >> 16), la = r1.x & 0xFFFF;
+          // nodes a, b are (ja, la), (ja, la + 1); their mirrors (ja, half - la), (ja, half - la - 1).  half is even,
+          // so exactly one of the two adjacent pairs starts 16-byte aligned: that one is one 16-byte store
+          T2* prow = Pol + (int64_t)ja * half;
+          if (la & 1) {
+            prow[la] = aa;
+            prow[la + 1] = ab;
+            *reinterpret_cast<float4*>(prow + (half - la - 1)) = make_float4(mb.x, mb.y, ma.x, ma.y);
+          } else {
+            *reinterpret_cast<float4*>(prow + la) = make_float4(aa.x, aa.y, ab.x, ab.y);
+            prow[half - la] = ma;
+            prow[half - la - 1] = mb;
+          }
         }
       }
       const int nb = pp.phase_node_begin[ph], ne = pp.phase_node_begin[ph + 1];

@@ -393,6 +393,7 @@ fbspca_status build_host_plan(Plan& P) {
   std::vector<char> in_quad(size_t(P.n_xi) * (half + 1), 0);
   // measured on B200 (C3): quads cut the gather's shared wavefronts 12 % but ran 2-4 % slower (more registers: spills in
   // the ring pass, more bank conflicts among the fewer doubles) -- kept behind FBSPCA_QUADS=1 for experiments
+  // (the kernel's quad loop is compiled only with -DFBSPCA_QUAD_GATHER)
   const bool quads = doubles && getenv("FBSPCA_QUADS") && atoi(getenv("FBSPCA_QUADS")) == 1;
   if (quads)
     for (int j = 0; j + 1 < P.n_xi; j += 2)
