@@ -34,8 +34,51 @@ __device__ __forceinline__ double2 rfma(double w, double2 g, double2 acc) {
   return {fma(w, g.x, acc.x), fma(w, g.y, acc.y)};
 }
 
+// packed fp32 complex add / subtract (add.rn.f32x2 / sub.rn.f32x2 = SASS FADD2: one instruction per complex op)
+__device__ __forceinline__ float2 padd(float2 a, float2 b) {
+  unsigned long long r, x, y;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(b.x), "f"(b.y));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+  float2 o;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+  return o;
+}
+__device__ __forceinline__ float2 psub(float2 a, float2 b) {
+  unsigned long long r, x, y;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(b.x), "f"(b.y));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+  float2 o;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+  return o;
+}
+
 // ---------------------------------------------------------------- small forward DFTs (e^{-2 pi i})
 template <typename T2, int R> struct Dft;
+// fp32 radix-4 / radix-8 butterflies with packed adds (the FFT phases are issue-bound)
+template <> struct Dft<float2, 4> {
+  __device__ __forceinline__ static void run(float2* v) {
+    const float2 s0 = padd(v[0], v[2]), d0 = psub(v[0], v[2]);
+    const float2 s1 = padd(v[1], v[3]), d1 = mul_mi(psub(v[1], v[3]));
+    v[0] = padd(s0, s1); v[2] = psub(s0, s1);
+    v[1] = padd(d0, d1); v[3] = psub(d0, d1);
+  }
+};
+template <> struct Dft<float2, 8> {
+  __device__ __forceinline__ static void run(float2* v) {
+    const float h = 0.70710678118654752440f;
+    float2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+    Dft<float2, 4>::run(e); Dft<float2, 4>::run(o);
+    const float2 t1 = {h * (o[1].x + o[1].y), h * (o[1].y - o[1].x)};
+    const float2 t2 = mul_mi(o[2]);
+    const float2 t3 = {h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y)};
+    v[0] = padd(e[0], o[0]); v[4] = psub(e[0], o[0]);
+    v[1] = padd(e[1], t1);   v[5] = psub(e[1], t1);
+    v[2] = padd(e[2], t2);   v[6] = psub(e[2], t2);
+    v[3] = padd(e[3], t3);   v[7] = psub(e[3], t3);
+  }
+};
 template <typename T2> struct Dft<T2, 2> {
   __device__ __forceinline__ static void run(T2* v) { T2 a = v[0]; v[0] = cadd(a, v[1]); v[1] = csub(a, v[1]); }
 };

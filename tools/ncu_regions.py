@@ -4,9 +4,9 @@ other files inherit the caller's region).  usage: python tools/ncu_regions.py mi
 import csv
 import sys
 
-REGIONS = [  # (first kernels_polar.cu line, name) -- see kernels_polar.cu
-    (0, "setup"), (150, "image/row FFT"), (205, "col fill"), (225, "col FFT"), (243, "gather doubles"),
-    (300, "gather singles"), (350, "ring FFT"), (520, "write-out"), (580, "tail")]
+REGIONS = [  # (first kernels_polar.cu line, name) -- kernels_polar.cu as of round 2
+    (0, "setup"), (160, "image/row FFT"), (208, "col fill"), (228, "col FFT"), (246, "gather doubles"),
+    (370, "gather singles"), (420, "ring FFT"), (600, "write-out"), (650, "tail")]
 
 
 def region_of(line):
