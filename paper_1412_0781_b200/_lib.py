@@ -7,7 +7,8 @@ import glob
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfbspca.so")
+# FBSPCA_LIB: load a variant build instead (A/B experiments, paper_1412_0781_b200/build.py --lib ... -D ...)
+LIB_PATH = os.environ.get("FBSPCA_LIB") or os.path.join(_HERE, "lib", "libfbspca.so")
 
 _lib = None
 

@@ -44,20 +44,24 @@ def _sidecar(path: str) -> str | None:
         return None
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    objdir = os.path.join(PKG, "build")
+def build(force: bool = False, verbose: bool = False, lib: str | None = None, defines: tuple = ()) -> str:
+    """Build (if stale) the library.  `lib` / `defines` build a variant elsewhere (A/B experiments: e.g.
+    lib=".../lib_alt/libfbspca.so", defines=("FBSPCA_TW_RECURRENCE=1",)), loaded with FBSPCA_LIB=<path>."""
+    LIB_ = lib or LIB
+    extra = [f"-D{d}" for d in defines]
+    objdir = os.path.join(PKG, "build" if not defines else "build_" + hashlib.sha256(" ".join(extra).encode()).hexdigest()[:8])
     os.makedirs(objdir, exist_ok=True)
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
+    os.makedirs(os.path.dirname(LIB_), exist_ok=True)
     hdrs = [os.path.join(PKG, h) for h in HDR]
-    shash = source_hash()
-    if not force and os.path.exists(LIB) and _sidecar(LIB) == shash:
-        return LIB                       # built from exactly these sources (objects need not be present)
+    shash = _digest([os.path.join(PKG, s) for s in SRC] + hdrs, FLAGS + extra)
+    if not force and os.path.exists(LIB_) and _sidecar(LIB_) == shash:
+        return LIB_                      # built from exactly these sources (objects need not be present)
     procs, objs = [], []
     for s in SRC:
         src = os.path.join(PKG, s)
         obj = os.path.join(objdir, os.path.basename(s) + ".o")
         objs.append(obj)
-        flags = FLAGS + ([f'-DFBSPCA_SRC_HASH="{shash}"'] if s.endswith("capi.cu") else [])
+        flags = FLAGS + extra + ([f'-DFBSPCA_SRC_HASH="{shash}"'] if s.endswith("capi.cu") else [])
         want = _digest([src] + hdrs, flags)
         if force or not os.path.exists(obj) or _sidecar(obj) != want:
             cmd = [NVCC] + flags + ["-c", src, "-o", obj]
@@ -70,12 +74,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
         open(obj + ".hash", "w").write(want + "\n")
         if verbose:
             sys.stdout.write(open(obj + ".log").read())
-    if force or procs or not os.path.exists(LIB) or _sidecar(LIB) != shash:
-        cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs + ["-ldl"]
+    if force or procs or not os.path.exists(LIB_) or _sidecar(LIB_) != shash:
+        cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB_] + objs + ["-ldl"]
         subprocess.check_call(cmd)
-        open(LIB + ".hash", "w").write(shash + "\n")
-    return LIB
+        open(LIB_ + ".hash", "w").write(shash + "\n")
+    return LIB_
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("--lib", default=None, help="output path of a variant library")
+    ap.add_argument("-D", action="append", default=[], help="extra preprocessor define for a variant")
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.v, lib=a.lib, defines=tuple(a.D)))

@@ -151,6 +151,11 @@ template <int GS> __device__ __forceinline__ void gsync(int bar) {
   else asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(GS) : "memory");
 }
 
+// fp32 stage twiddles from one table load + products (fewer shared loads, more FP instructions) or R - 1 table loads;
+// measured on B200 (tools/ab_bench.sh, same box ABAB): products 54.5 ms vs table 55.5 ms polar at C3 -> products
+#ifndef FBSPCA_TW_RECURRENCE
+#define FBSPCA_TW_RECURRENCE 1
+#endif
 // w[r] = w[1]^r, r = 2..R-1, from w[1] by at most three multiplications deep
 template <typename T2, int R>
 __device__ __forceinline__ void twiddle_powers(T2* w) {
@@ -176,7 +181,7 @@ __device__ __forceinline__ void cstage(Ld ld, St st, const T2* __restrict__ tws,
         else v[r] = ld(j + r * NB);
       }
       const int jm = j % Ns;                      // compile-time Ns: a mask for powers of two
-      if constexpr (Ns > 1 && sizeof(v[0].x) == 4 && R >= 3) {
+      if constexpr (Ns > 1 && sizeof(v[0].x) == 4 && R >= 3 && FBSPCA_TW_RECURRENCE) {
         // fp32: one table load per butterfly; w^r for r >= 2 by products of w (depth <= 3 multiplications,
         // relative error <= ~4e-7, below the fp32 FFT's own ~log2(N) u).  Saves R - 2 shared loads.
         T2 w[R];
