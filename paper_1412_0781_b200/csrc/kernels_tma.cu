@@ -752,6 +752,7 @@ static cudaError_t launch_cov_tma_t(const Plan& P, const MapSet& ta, K5Args& a, 
   const int per_sm = env ? std::max(1, std::min(2, atoi(env))) : 2;
   const int budget = (per_sm == 2 ? 113 : 227) * 1024;
   a.ck = K5_CK;                                            // fewer chunks per stage when a tile is 32 KB
+  if (const char* e = getenv("FBSPCA_K5_CK")) a.ck = std::max(1, std::min(8, atoi(e)));   // A/B knob
   while (a.ck > 1 && 2 * a.ck * std::max(128, 2 * RR) * ROWB > budget - fixed) a.ck /= 2;
   const int stage = a.ck * std::max(128, 2 * RR) * ROWB;
   a.stages = std::max(2, std::min(8, (budget - fixed) / stage));
@@ -777,6 +778,7 @@ cudaError_t launch_cov_tma(const Plan& P, const void* d_coeffs, int64_t ld, int6
   K5Args a;
   a.k_max = P.k_max; a.k_lo = kb + 1; a.chunk = kCovChunk; a.nchunk = int((nb + kCovChunk - 1) / kCovChunk);
   a.drain = 128; a.i0 = i0; a.nb = nb; a.ld = ld; a.p = P.d_p; a.coef_off = P.d_coef_off; a.blk_off = P.d_blk_off;
+  if (const char* e = getenv("FBSPCA_K5_DRAIN")) a.drain = std::max(16, std::min(512, atoi(e)));   // A/B knob
   a.scratch = P.d_cov_scratch; a.scratch_stride = P.blk_off[P.k_max + 1] + P.p[0] + 1;
   if (kb > 0) {
     K5Args b = a;
