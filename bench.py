@@ -138,13 +138,13 @@ def cpu_baseline(cfg, seconds_target=15.0):
     t0 = time.perf_counter()
     O.block_covariance(O.expand(imgs, basis))
     per = (time.perf_counter() - t0) / 2
-    m = max(2, min(64, int(seconds_target / max(per, 1e-3))))
+    m = max(2, min(512, int(seconds_target / max(per, 1e-3))))
     imgs = synth.blob_images(cfg, 0, m, sigma_n=sig).double().numpy()
     t0 = time.perf_counter()
     O.block_covariance(O.expand(imgs, basis))
     dt = time.perf_counter() - t0
-    if dt < 0.5 * seconds_target and m < 64:     # the 2-image probe carries per-call costs: size once more
-        m = max(m + 1, min(64, int(m * seconds_target / dt)))
+    if dt < 0.5 * seconds_target and m < 512:    # the 2-image probe carries per-call costs: size once more
+        m = max(m + 1, min(512, int(m * seconds_target / dt)))
         imgs = synth.blob_images(cfg, 0, m, sigma_n=sig).double().numpy()
         t0 = time.perf_counter()
         O.block_covariance(O.expand(imgs, basis))
@@ -163,7 +163,7 @@ def run_reference(args, cfg, rank):
         return
     basis = O.build_basis(cfg["c"], cfg["R"])
     sig = synth.blobs.noise_sigma(cfg)
-    m = 4 if cfg["L"] >= 128 else 32
+    m = 32 if cfg["L"] <= 128 else 4          # C3: 32 images (~1.5 s of host work) per step
     imgs = synth.blob_images(cfg, 0, m, sigma_n=sig).double().numpy()
     for _ in range(args.warmup):
         O.block_covariance(O.expand(imgs, basis))
