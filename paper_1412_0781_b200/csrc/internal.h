@@ -187,6 +187,7 @@ int polar_max_smem();
 cudaError_t launch_radial_tma(const Plan& P, int64_t nb, int64_t i0, int64_t ld, void* d_coeffs, cudaStream_t s);
 cudaError_t launch_cov_tma(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb, cudaStream_t s);
 cudaError_t launch_cov_k0(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb, cudaStream_t s);
+int cov_tma_chunk();                    // images per split-K chunk of the tensor-core K5 (a multiple of kCovChunk)
 int fft_values_per_lane(const FftPlan& f);
 int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps, int nk);
 

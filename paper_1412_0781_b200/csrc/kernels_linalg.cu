@@ -197,12 +197,15 @@ __global__ void cov_reduce_kernel(const double* __restrict__ scratch, int64_t st
 cudaError_t launch_cov_accum(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb,
                              double* d_partial, cudaStream_t s) {
   const int nt = (P.p[0] + 63) / 64;
-  const int nchunk = (int)((nb + kCovChunk - 1) / kCovChunk);
+  const bool tc_ok = P.dt == FBSPCA_F32 && P.use_tc && P.k_max >= 1 && ((P.p[1] + 15) & ~15) <= 256 && (ld % 2) == 0;
+  // images per split-K chunk: kCovChunk (SIMT), cov_tma_chunk() (tensor path)
+  const int chunk = tc_ok ? cov_tma_chunk() : kCovChunk;
+  const int nchunk = (int)((nb + chunk - 1) / chunk);
   if (nchunk > kCovMaxChunks) return cudaErrorInvalidValue;
   const int64_t total = P.blk_off[P.k_max + 1] + P.p[0] + 1;
   dim3 grid((unsigned)(P.k_max + 1), (unsigned)(nt * (nt + 1) / 2), (unsigned)nchunk);
   // k >= 1 on tcgen05 for p_1 <= 256 (p_k > 128: the big-block kernel, kernels_tma.cu)
-  const bool tc = P.dt == FBSPCA_F32 && P.use_tc && P.k_max >= 1 && ((P.p[1] + 15) & ~15) <= 256 && (ld % 2) == 0;
+  const bool tc = tc_ok;
   if (tc) {
     // k >= 1 on the tensor cores (TMA-fed, persistent); k = 0 (uncentred, mean^2/var ~ 10: F9) in fp64 on the
     // CUDA cores, forked onto the plan's side stream so the two overlap

@@ -765,7 +765,19 @@ static cudaError_t launch_cov_tma_t(const Plan& P, const MapSet& ta, K5Args& a, 
   return cudaGetLastError();
 }
 
-// k >= 1 of the batch [i0, i0 + nb) into scratch[chunk] (chunks of kCovChunk images); k = 0 is not touched.
+// images per tensor-core split-K chunk: kCovChunk x FBSPCA_K5_CHUNKS (1, 2 or 4; default 4: A/B on B200, C3 K5 2.53 ->
+// 2.35 ms -- fewer per-item epilogues; partial-sum error unchanged at 1.8e-6).  TMEM drains every `drain` images into
+// fp32 registers, so a chunk's register sums add chunk / drain drained groups (32 at the default)
+int cov_tma_chunk() {
+  static const int m = [] {
+    const char* e = getenv("FBSPCA_K5_CHUNKS");
+    const int v = e ? atoi(e) : 4;
+    return (v == 1 || v == 2) ? v : 4;
+  }();
+  return kCovChunk * m;
+}
+
+// k >= 1 of the batch [i0, i0 + nb) into scratch[chunk] (chunks of cov_tma_chunk() images); k = 0 is not touched.
 cudaError_t launch_cov_tma(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb, cudaStream_t s) {
   if (P.k_max < 1) return cudaSuccess;
   if (((P.p[1] + 15) & ~15) > 256) return cudaErrorInvalidValue;   // p_k > 256: not on this path
@@ -776,7 +788,8 @@ cudaError_t launch_cov_tma(const Plan& P, const void* d_coeffs, int64_t ld, int6
   for (int i = 0; i < 4; ++i)
     if (!make_map(&ta.m[i], d_coeffs, P.coef_off[P.k_max + 1], 2 * ld, 2 * ld, 16 << i)) return cudaErrorInvalidValue;
   K5Args a;
-  a.k_max = P.k_max; a.k_lo = kb + 1; a.chunk = kCovChunk; a.nchunk = int((nb + kCovChunk - 1) / kCovChunk);
+  const int chunk = cov_tma_chunk();
+  a.k_max = P.k_max; a.k_lo = kb + 1; a.chunk = chunk; a.nchunk = int((nb + chunk - 1) / chunk);
   a.drain = 128; a.i0 = i0; a.nb = nb; a.ld = ld; a.p = P.d_p; a.coef_off = P.d_coef_off; a.blk_off = P.d_blk_off;
   if (const char* e = getenv("FBSPCA_K5_DRAIN")) a.drain = std::max(16, std::min(512, atoi(e)));   // A/B knob
   a.scratch = P.d_cov_scratch; a.scratch_stride = P.blk_off[P.k_max + 1] + P.p[0] + 1;
