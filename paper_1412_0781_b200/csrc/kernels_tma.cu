@@ -332,6 +332,11 @@ struct K5Args {
   int64_t scratch_stride;
 };
 
+// K-chunk stacking (RR <= 64): a 128-row tile holds G = 128 / (2 b) K-chunks of block k, [x; lo] each, so ONE MMA
+// (M = N = 128) covers G chunks: D = tile tile^T, of which the G diagonal 2b x 2b blocks are the wanted
+// [x; lo] [x; lo]^T of their chunks (the off-diagonal blocks pair different images and are never read).  Small p_k
+// no longer costs a full 64-cycle M = 128 MMA per 32 image-columns.  Warp w drains its rows' diagonal block
+// (group (32 w) / (2 b): uniform per warp); the G groups are summed through shared memory in the epilogue.
 template <int RR>   // register accumulators per thread (= largest box b of k >= 1)
 __global__ void __launch_bounds__(192, RR <= 64 ? 2 : 1)
 cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
@@ -340,7 +345,9 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
   unsigned char* sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u);
   const int CK = args.ck;
   const int NS = args.stages;
-  const uint32_t tile_bytes = uint32_t(max(128, 2 * RR)) * ROWB;   // the M = 128 A operand reads 128 rows
+  constexpr int TROWS = RR <= 64 ? 128 : 2 * RR;                   // tile rows (the M = 128 A operand reads 128)
+  constexpr int AW = TROWS;                                         // accumulator columns (N of a stacked tile)
+  const uint32_t tile_bytes = uint32_t(TROWS) * ROWB;
   const uint32_t stage_bytes = CK * tile_bytes;
   float* tr = reinterpret_cast<float*>(sm + NS * stage_bytes);      // RR x (RR + 1) epilogue transpose
   uint64_t* full = reinterpret_cast<uint64_t*>(tr + RR * (RR + 1));
@@ -350,7 +357,7 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
   uint64_t* accempty = accfull + 2;                                 // 2
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int tcols = pow2_cols(4 * RR);                              // two accumulators of 2 b columns
+  const int tcols = pow2_cols(2 * AW);                              // two accumulators
 
   if (warp == 0) tmem_alloc(tmem_slot, tcols);
   if (tid == 0) {
@@ -363,29 +370,38 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
   const int n_items = (args.k_max - args.k_lo + 1) * args.nchunk;
-  const int st_per_group = max(1, (2 * args.drain) / (KC * CK));   // stages per drain group
-  auto item_geom = [&](int item, int& k, int& ch, int& nkc) {
-    k = args.k_lo + item / args.nchunk; ch = item - (k - args.k_lo) * args.nchunk;
-    const int64_t img0 = args.i0 + int64_t(ch) * args.chunk;
+  // per item: b (box rows), G (chunks per tile), nkc (K chunks), ntile, nst (stages), spg (stages per drain group)
+  struct Geo { int k, ch, b, G, nkc, ntile, nst, spg; };
+  auto item_geom = [&](int item) {
+    Geo e;
+    e.k = args.k_lo + item / args.nchunk; e.ch = item - (e.k - args.k_lo) * args.nchunk;
+    const int64_t img0 = args.i0 + int64_t(e.ch) * args.chunk;
     const int ncols = int(2 * min(int64_t(args.chunk), args.i0 + args.nb - img0));
-    nkc = (ncols + KC - 1) / KC;
+    e.nkc = (ncols + KC - 1) / KC;
+    e.b = 16 << box_idx((args.p[e.k] + 15) & ~15);
+    e.G = RR <= 64 ? TROWS / (2 * e.b) : 1;
+    e.ntile = (e.nkc + e.G - 1) / e.G;
+    e.nst = (e.ntile + CK - 1) / CK;
+    e.spg = max(1, (2 * args.drain) / (KC * CK * e.G));
+    return e;
   };
 
   if (warp == 4) {                                                  // ---- TMA producer
     if (lane == 0) {
       int it = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-        int k, ch, nkc;
-        item_geom(item, k, ch, nkc);
-        const int bi = box_idx((args.p[k] + 15) & ~15);
-        const int col0 = int(2 * (args.i0 + int64_t(ch) * args.chunk));
-        const int row0 = int(args.coef_off[k]);
-        for (int kc0 = 0; kc0 < nkc; kc0 += CK, ++it) {
-          const int s = it % NS, nc = min(CK, nkc - kc0);
+        const Geo e = item_geom(item);
+        const int bi = box_idx(e.b);
+        const int col0 = int(2 * (args.i0 + int64_t(e.ch) * args.chunk));
+        const int row0 = int(args.coef_off[e.k]);
+        for (int si = 0; si < e.nst; ++si, ++it) {
+          const int s = it % NS, nt = min(CK, e.ntile - si * CK);
+          const int kc0 = si * CK * e.G, nkc_here = min(nt * e.G, e.nkc - kc0);
           bar_wait(&empty[s], ((it / NS) & 1) ^ 1);
-          bar_expect_tx(&full[s], uint32_t(nc) * (16u << bi) * ROWB);
-          for (int c = 0; c < nc; ++c)
-            tma_2d(sm + s * stage_bytes + c * tile_bytes, &tm_a.m[bi], col0 + (kc0 + c) * KC, row0, &full[s]);
+          bar_expect_tx(&full[s], uint32_t(nkc_here) * uint32_t(e.b) * ROWB);
+          for (int u = 0; u < nkc_here; ++u)                        // chunk kc0 + u -> tile u / G, group u % G
+            tma_2d(sm + s * stage_bytes + (u / e.G) * tile_bytes + (u % e.G) * 2 * e.b * ROWB, &tm_a.m[bi],
+                   col0 + (kc0 + u) * KC, row0, &full[s]);
         }
       }
     }
@@ -395,24 +411,21 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
     if (lane == 0) {
       int it = 0, g = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-        int k, ch, nkc;
-        item_geom(item, k, ch, nkc);
-        const int b = 16 << box_idx((args.p[k] + 15) & ~15);
-        const uint32_t idesc = idesc_tf32(128, 2 * b);
-        const int nst = (nkc + CK - 1) / CK;
-        for (int si = 0; si < nst; ++si, ++it) {
-          const bool first = (si % st_per_group) == 0;
-          const bool last = (si % st_per_group) == st_per_group - 1 || si == nst - 1;
+        const Geo e = item_geom(item);
+        const uint32_t idesc = idesc_tf32(128, e.G * 2 * e.b);
+        for (int si = 0; si < e.nst; ++si, ++it) {
+          const bool first = (si % e.spg) == 0;
+          const bool last = (si % e.spg) == e.spg - 1 || si == e.nst - 1;
           const int a = g & 1;
-          const uint32_t d = tmem + uint32_t(a * 2 * RR);
+          const uint32_t d = tmem + uint32_t(a * AW);
           if (first) {
             bar_wait(&accempty[a], ((g >> 1) & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
           }
-          const int s = it % NS, nc = min(CK, nkc - si * CK);
+          const int s = it % NS, nt = min(CK, e.ntile - si * CK);
           bar_wait(&loready[s], (it / NS) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          for (int c = 0; c < nc; ++c) {
+          for (int c = 0; c < nt; ++c) {
             const uint32_t x = su32(sm + s * stage_bytes + c * tile_bytes);
 #pragma unroll
             for (int s4 = 0; s4 < KC / 8; ++s4) {
@@ -431,11 +444,11 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
   const int q = 32 * warp + lane;
   int it = 0, g = 0;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-    int k, ch, nkc;
-    item_geom(item, k, ch, nkc);
+    const Geo e = item_geom(item);
+    const int k = e.k, ch = e.ch, b = e.b;
     const int pk = args.p[k];
-    const int b = 16 << box_idx((pk + 15) & ~15);
-    const int nst = (nkc + CK - 1) / CK;
+    const int gw = RR <= 64 ? (32 * warp) / (2 * b) : 0;   // this warp's diagonal block (uniform per warp)
+    const int qq = q - 2 * b * gw;                         // row within the block (< b: an x row)
     float acc[RR];
 #pragma unroll
     for (int i = 0; i < RR; ++i) acc[i] = 0.f;
@@ -443,7 +456,7 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
       const int a = gg & 1;
       bar_wait(&accfull[a], (gg >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t tb = tmem + (uint32_t(32 * warp) << 16) + uint32_t(a * 2 * RR);
+      const uint32_t tb = tmem + (uint32_t(32 * warp) << 16) + uint32_t(a * AW + 2 * b * gw);
       // 16 columns of X and Y in flight per wait (b is a power of two >= 16; few registers: 2 CTAs per SM)
 #pragma unroll
       for (int c1 = 0; c1 < RR; c1 += 16) {
@@ -456,7 +469,7 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
           for (int i = 0; i < 16; ++i) {
             const int c = c1 + i;
             const float xv = __uint_as_float(xr[i]), yv = __uint_as_float(yr[i]);
-            acc[c] += c > q ? yv : c == q ? xv + 2.f * yv : xv + yv;
+            acc[c] += c > qq ? yv : c == qq ? xv + 2.f * yv : xv + yv;
           }
         }
       }
@@ -464,25 +477,38 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
       bar_arrive(&accempty[a]);
     };
     int pending = -1;
-    for (int si = 0; si < nst; ++si, ++it) {
-      const int s = it % NS, nc = min(CK, nkc - si * CK);
+    for (int si = 0; si < e.nst; ++si, ++it) {
+      const int s = it % NS, nt = min(CK, e.ntile - si * CK);
+      const int kc0 = si * CK * e.G, nkc_here = min(nt * e.G, e.nkc - kc0);
       unsigned char* st = sm + s * stage_bytes;
       bar_wait(&full[s], (it / NS) & 1);
-      for (int c = 0; c < nc; ++c) make_lo(st + c * tile_bytes, st + c * tile_bytes + b * ROWB, b * ROWB, tid);
+      for (int u = 0; u < nt * e.G; ++u) {
+        unsigned char* xu = st + (u / e.G) * tile_bytes + (u % e.G) * 2 * b * ROWB;
+        if (u >= nkc_here) {                                 // ragged end of the item: no chunk loaded, zero it
+          for (int i = tid; i < b * KC; i += 128) reinterpret_cast<float*>(xu)[i] = 0.f;
+          named_sync(1, 128);
+        }
+        make_lo(xu, xu + b * ROWB, b * ROWB, tid);
+      }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       bar_arrive(&loready[s]);
-      const bool last = (si % st_per_group) == st_per_group - 1 || si == nst - 1;
+      const bool last = (si % e.spg) == e.spg - 1 || si == e.nst - 1;
       if (last) {                                            // drain the previous group while this one runs
         if (pending >= 0) drain(pending);
         pending = g++;
       }
     }
     drain(pending);
-    // S = acc_q[q'] + acc_q'[q] through shared memory, fp64 upper triangle into scratch[chunk]
-    named_sync(1, 128);
-    if (q < RR) {
+    // S = acc_q[q'] + acc_q'[q] through shared memory (summing the G stacked groups), fp64 upper triangle
+    for (int gg = 0; gg < e.G; ++gg) {
+      named_sync(1, 128);
+      if (gw == gg && qq < b && qq < RR) {
 #pragma unroll
-      for (int c = 0; c < RR; ++c) tr[q * (RR + 1) + c] = acc[c];
+        for (int c = 0; c < RR; ++c) {
+          if (gg == 0) tr[qq * (RR + 1) + c] = acc[c];
+          else tr[qq * (RR + 1) + c] += acc[c];
+        }
+      }
     }
     named_sync(1, 128);
     double* dst = args.scratch + int64_t(ch) * args.scratch_stride + args.blk_off[k];
@@ -495,7 +521,6 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
   named_sync(1, 128);
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
 }
-
 
 // ---------------------------------------------------------------- K5, blocks with 128 < p_k <= 256 (C5, T3)
 // S_k in 128 x 128 output blocks (m, n) in {(0,0), (0,1), (1,1)} of the row halves x_0 = rows 0..127, x_1 = rows
