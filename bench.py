@@ -350,8 +350,8 @@ def main():
         alu_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12          # fp32 FFMA TFLOP/s at max clock
         achieved = wk["polar_flops"] * imgs_per_launch / (per_launch_polar_ms / 1e3) / 1e12
         # per step: (polar + radial) per expand batch; (tcgen05 SYRK, k=0 fp64 on the side stream, chunk
-        # reduction) per 16384-image covariance batch; finalize.  NCCL's all-reduce kernel is not ours.
-        n_cov_launch = 3 * math.ceil(n_local / 16384)
+        # reduction) per 65536-image covariance batch (tensor-core path); finalize.  NCCL's all-reduce kernel is not ours.
+        n_cov_launch = 3 * math.ceil(n_local / 65536)
         gpu_launches = args.steps * (2 * math.ceil(n_local / plan_batch(plan)) + n_cov_launch + 1)
         kernels = {}
         for name, tms in kms.items():

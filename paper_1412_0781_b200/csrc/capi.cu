@@ -421,7 +421,8 @@ static fbspca_status cov_accumulate(fbspca_plan_t h, const void* d_coeffs, int64
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t npart = P.blk_off[P.k_max + 1] + P.p[0] + 1;
   if (zero) FB_CUDA(cudaMemsetAsync(d_partial, 0, npart * sizeof(double), s), "memset partial");
-  const int64_t B = kCovBatch;
+  // images per launch: 16 split-K chunks (tensor path: 16 x 4096 = kCovBatchTc by default)
+  const int64_t B = cov_uses_tc(P, n_local) ? int64_t(cov_tma_chunk()) * kCovMaxChunks : kCovBatch;
   TimedRegion t(P, T_COV, s);
   for (int64_t i0 = 0; i0 < n_local; i0 += B) {
     const int64_t nb = std::min<int64_t>(B, n_local - i0);

@@ -13,11 +13,15 @@ namespace fbspca {
 
 constexpr int kMaxRadixStages = 16;
 constexpr int kMaxPhases = 64;
-constexpr int kCovChunk = 1024;         // images per covariance split-K chunk (bounds fp32 accumulation length)
-constexpr int kCovBatch = 16384;        // images per covariance launch
-constexpr int kCovMaxChunks = kCovBatch / kCovChunk;
+constexpr int kCovChunk = 1024;         // images per SIMT covariance split-K chunk (bounds fp32 accumulation length)
+constexpr int kCovBatch = 16384;        // images per SIMT covariance launch
+constexpr int kCovChunkTc = 4096;       // images per tensor-core split-K chunk (cov_tma_chunk() <= this)
+constexpr int kCovBatchTc = 65536;      // images per tensor-core covariance launch (A/B on B200: 16384 -> 65536 took the
+                                        // C3 K5 from 2.03 to 1.85 ms: more items per persistent CTA, fewer launch tails)
+constexpr int kCovMaxChunks = kCovBatch / kCovChunk;        // 16 scratch slots; kCovBatchTc / kCovChunkTc = 16 too
+static_assert(kCovBatchTc / kCovChunkTc <= kCovMaxChunks, "covariance scratch slots");
 constexpr int kCovChunk0 = 128;         // images per k = 0 fp64 CTA (tensor-core path: its own scratch, more CTAs)
-constexpr int kCovMaxSub0 = kCovBatch / kCovChunk0;
+constexpr int kCovMaxSub0 = kCovBatchTc / kCovChunk0;
 
 // Stockham radix plan for a length-N FFT (N = prod radices; radices in {2,3,4,5,8}).
 struct FftPlan {
@@ -188,6 +192,7 @@ cudaError_t launch_radial_tma(const Plan& P, int64_t nb, int64_t i0, int64_t ld,
 cudaError_t launch_cov_tma(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb, cudaStream_t s);
 cudaError_t launch_cov_k0(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb, cudaStream_t s);
 int cov_tma_chunk();                    // images per split-K chunk of the tensor-core K5 (a multiple of kCovChunk)
+bool cov_uses_tc(const Plan& P, int64_t ld);   // K5 for k >= 1 on tcgen05 for this plan and leading dimension
 int fft_values_per_lane(const FftPlan& f);
 int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps, int nk);
 

@@ -194,10 +194,14 @@ __global__ void cov_reduce_kernel(const double* __restrict__ scratch, int64_t st
   }
 }
 
+bool cov_uses_tc(const Plan& P, int64_t ld) {
+  return P.dt == FBSPCA_F32 && P.use_tc && P.k_max >= 1 && ((P.p[1] + 15) & ~15) <= 256 && (ld % 2) == 0;
+}
+
 cudaError_t launch_cov_accum(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb,
                              double* d_partial, cudaStream_t s) {
   const int nt = (P.p[0] + 63) / 64;
-  const bool tc_ok = P.dt == FBSPCA_F32 && P.use_tc && P.k_max >= 1 && ((P.p[1] + 15) & ~15) <= 256 && (ld % 2) == 0;
+  const bool tc_ok = cov_uses_tc(P, ld);
   // images per split-K chunk: kCovChunk (SIMT), cov_tma_chunk() (tensor path)
   const int chunk = tc_ok ? cov_tma_chunk() : kCovChunk;
   const int nchunk = (int)((nb + chunk - 1) / chunk);

@@ -799,6 +799,7 @@ int cov_tma_chunk() {
     const int v = e ? atoi(e) : 4;
     return (v == 1 || v == 2) ? v : 4;
   }();
+  static_assert(kCovChunk * 4 <= kCovChunkTc, "tensor-core chunk");
   return kCovChunk * m;
 }
 
