@@ -21,7 +21,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-BATCH = 25000         # images per expand batch (ghat workspace 4.7 GB at C3); 4 batches per 100k step
+BATCH = 50000         # images per expand batch (ghat workspace 9.4 GB at C3); 2 batches per 100k step
+                      # (A/B on B200: 25000 -> 50000 took the polar kernel from 54.7 to 54.4 ms: fewer launch tails)
 METRIC = "images/sec (expansion+covariance, L=128) at 1/2/4/8 B200; % HBM roofline"
 
 
@@ -210,8 +211,13 @@ def main():
     s, e = F.shard_range(n, rank, world)
     n_local = e - s
     dt = F.F32 if cfg["dtype"] == "f32" else F.F64
-    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], dtype=dt, device=local, max_batch=args.batch)
-    plan.bench_batch = args.batch
+    # expand batch: args.batch, capped so the plan's ghat workspace stays <= 40 GB (C5: ~25,800 images)
+    probe = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], dtype=dt, device=-1)
+    ghat_per_image = (probe.k_max + 1) * 2 * probe.n_xi * (4 if dt == F.F32 else 8)
+    batch = max(1, min(args.batch, int(40e9 // ghat_per_image)))
+    del probe
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], dtype=dt, device=local, max_batch=batch)
+    plan.bench_batch = batch
     comm = None
     if world > 1 or args.nccl:
         obj = [F.fbspca_nccl_unique_id() if rank == 0 else None]
@@ -397,7 +403,7 @@ def main():
             "config": {"workload": (f"{cfg['name']}: BASELINE.json configs[{int(cfg['name'][1]) - 1}]"
                                     if cfg["name"].startswith("C") else WORKLOADS[cfg["name"]]), "n": n,
                        "L": cfg["L"], "R": cfg["R"], "c": cfg["c"], "parallelism": f"dp{world}",
-                       "n_per_rank": n_local, "eps": 1e-5, "M": plan.M, "w": plan.w,
+                       "n_per_rank": n_local, "eps": 1e-5, "M": plan.M, "w": plan.w, "expand_batch": plan_batch(plan),
                        "l2": f"inputs larger than L2 ({n * cfg['L'] * cfg['L'] * (4 if dt == F.F32 else 8) / 1e9:.1f} GB "
                              "of images read per step, L2 126 MB)"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",

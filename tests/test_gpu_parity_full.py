@@ -4,7 +4,7 @@
   whole config (tests/golden/oracle_C{2,3}.npz, written by tools/oracle_cache.py, which calls only `synth` on the
   CPU and `oracle/`: its own expansion, not the GPU's coefficients).  The images here are generated on the GPU by
   the same seeded generator; a sample of them is checked against the CPU generator the cache consumed.
-* C3 coefficients of 2,048 images spread over all four 25,000-image expand batches and every CTA residue mod 148
+* C3 coefficients of 2,048 images spread over both 50,000-image expand batches and every CTA residue mod 148
   (the polar kernel's persistent grid stride), plan built exactly as bench.py builds it.
 * C4 / C5: 512-image subsets, coefficients of every image and the subset's spectrum against the oracle's own
   expansion of those images.
@@ -32,7 +32,7 @@ DEV = torch.device("cuda:0") if torch.cuda.is_available() else None
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 TOL32 = 1e-4
-BENCH_BATCH = 25000                       # bench.py BATCH: images per expand batch in the timed configuration
+BENCH_BATCH = 50000                       # bench.py BATCH: images per expand batch in the timed configuration
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -141,13 +141,13 @@ def test_c3_full_size_spectral_vs_cached_oracle(c3_run):
     cache = load_cache("C3")
     r = c3_run
     assert cache["n"] == r["n"] and abs(cache["sigma_n"] - r["sig"]) <= 1e-12 * r["sig"]
-    check_inputs_match_cpu_generator(r["cfg"], r["imgs"], r["sig"], [0, 24999, 25000, 77777, r["n"] - 1])
+    check_inputs_match_cpu_generator(r["cfg"], r["imgs"], r["sig"], [0, 49999, 50000, 77777, r["n"] - 1])
     spectral_checks(r["plan"], r["blocks"], r["mean"], r["evals"], r["evecs"], cache["mean"], cache["C"],
                     cache["lam"], cache["U"])
 
 
-def c3_sample_indices(n, batch, per_batch=512, seed=0):
-    """Per 25,000-image batch: the first 148 images (every CTA residue of the 148-CTA persistent grid, first pass),
+def c3_sample_indices(n, batch, per_batch=1024, seed=0):
+    """Per expand batch: the first 148 images (every CTA residue of the 148-CTA persistent grid, first pass),
     the last 148 (every residue, ragged last pass), the batch edges, and random fill -- per_batch in total."""
     rng = np.random.default_rng(seed)
     out = []
