@@ -263,15 +263,18 @@ def _spectral_checks(plan, blocks, mean, evals, evecs, m_o, C_o, tol_c=1e-4):
 
 
 def test_c5_full_size_sampled_expansion():
-    """configs[4] at full size (50,000 images of 360 x 360) in bench.py's launch configuration (25,000-image
-    expand batches): the last image of each batch (the CTAs' ragged tail) against the fp64 oracle."""
+    """configs[4] at full size (50,000 images of 360 x 360) in bench.py's launch configuration (expand batches of
+    min(50,000, 40 GB of ghat) = 25,806 images): the first and last image of each batch (the CTAs' first and ragged
+    last pass) against the fp64 oracle."""
     cfg = synth.config("C5")
     n = cfg["n"]
     imgs = synth.blob_images(cfg, 0, n, device=DEV)
-    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=25000)
+    probe = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=-1)
+    batch = min(50000, int(40e9 // ((probe.k_max + 1) * 2 * probe.n_xi * 4)))
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=batch)
     coeffs = F.fbspca_expand(plan, imgs)
     torch.cuda.synchronize()
-    pick = [24999, n - 1]
+    pick = [0, batch - 1, batch, n - 1]
     sample = imgs[pick].double().cpu().numpy()
     got = coeffs[:, pick].cpu().numpy().astype(np.complex128)
     del imgs, coeffs
