@@ -150,9 +150,16 @@ def cpu_baseline(cfg, seconds_target=15.0):
         t0 = time.perf_counter()
         O.block_covariance(O.expand(imgs, basis))
         dt = time.perf_counter() - t0
-    return {"value": m / dt, "unit": "images/s", "cores": os.cpu_count(), "kind": "oracle",
+    import torch
+    return {"value": m / dt, "unit": "images/s", "cores": torch.get_num_threads(), "host_cpus": os.cpu_count(),
+            "kind": "oracle",
             "sample": f"first {m} images of {cfg['name']} (oracle: direct Fourier sum + FFT + GL + fp64 covariance), "
                       f"{dt:.1f} s on the host, numpy/BLAS threads = all cores"}
+
+
+def _threads():
+    import torch
+    return torch.get_num_threads()          # the oracle's BLAS / elementwise work runs on torch's CPU thread pool
 
 
 def run_reference(args, cfg, rank):
@@ -180,7 +187,8 @@ def run_reference(args, cfg, rank):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{cfg['name']} sample of {m} images (oracle, CPU)", "L": cfg["L"], "R": cfg["R"],
                        "c": cfg["c"], "n_sample": m},
-            "cpu_baseline": {"value": value, "unit": "images/s", "cores": os.cpu_count(), "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": "images/s", "cores": _threads(), "host_cpus": os.cpu_count(),
+                             "kind": "oracle",
                              "sample": f"{m} images of {cfg['name']} per step"},
             "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
