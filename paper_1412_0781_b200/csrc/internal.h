@@ -50,6 +50,8 @@ struct PolarParams {
   int img_off;                    // complex-element offset of the staged image in the region (-1: read global)
   int img_prefetch;               // 1: the next image is loaded (cp.async) during the angular pass
   int ring_pairs;                 // 1: n_theta = 2 M, rings transformed in pairs of M-point FFTs (K3)
+  int tmem_x;                     // 1: the second column phase's row-FFT columns are parked in TMEM, not in X (M = 256)
+  int tmem_g0, tmem_ng;           //    32-column groups g0 .. g0 + ng - 1 of the row pass hold them
   FftPlan fft_M, fft_theta;
   // device pointers (plan-owned)
   const void* deapod;             // L values (T): d(i) = 1/Phi(i/M), i = a - floor(L/2)

@@ -37,6 +37,20 @@ __device__ __forceinline__ void l2_discard(const void* base, size_t bytes, int t
     asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
 }
 
+// ---------------------------------------------------------------- TMEM as scratch (tcgen05.st / ld, 32x32b: each lane its row)
+__device__ __forceinline__ void tm_st4(uint32_t taddr, float a, float b, float c, float d) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};"
+               ::"r"(taddr), "r"(__float_as_uint(a)), "r"(__float_as_uint(b)), "r"(__float_as_uint(c)),
+                 "r"(__float_as_uint(d)) : "memory");
+}
+__device__ __forceinline__ float4 tm_ld4(uint32_t taddr) {
+  uint32_t r0, r1, r2, r3;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(taddr) : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return make_float4(__uint_as_float(r0), __uint_as_float(r1), __uint_as_float(r2), __uint_as_float(r3));
+}
+
 // ---------------------------------------------------------------- ES window weights
 // phi(d) = exp(beta (sqrt(1 - (d/hw)^2) - 1)), |d| <= hw.  fp32: MUFU sqrt.approx / ex2.approx
 // (relative error ~1e-7, far below the 1e-5 NUFFT budget); fp64: exact.
@@ -126,6 +140,23 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
   }
   __syncthreads();
 
+  // TMEM parking (pp.tmem_x, M = 256): warp w keeps its row pairs' second-phase columns in TMEM lanes 32 (w % 4) ..,
+  // columns 64 (w / 4) .. -- written by the row pass, read back by the same warp as the phase-1 fill (no L2 round trip)
+  __shared__ uint32_t tmem_slot;
+  uint32_t tmem_base = 0;
+  const bool use_tmem = (MC == 256) && pp.tmem_x;
+  if (use_tmem) {
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;"
+                   ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_slot))));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    tmem_base = tmem_slot;
+  }
+  const uint32_t tmem_mine = tmem_base + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(64 * (warp >> 2));
   T2* X = reinterpret_cast<T2*>(pp.xscratch) + (int64_t)blockIdx.x * pp.xscratch_stride;
   T2* Pol = reinterpret_cast<T2*>(pp.pscratch) + (int64_t)blockIdx.x * pp.pscratch_stride;
   const int ncx = pp.ncols_x, col_lo = pp.col_lo, S = pp.S;
@@ -181,8 +212,11 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         fft_any<T2, MC, true, FG>(pp.fft_M, ld, st, myA, myB, twM, glane, gbar);
         const int lo0 = pp.phase_lo[0], hi0 = lo0 + (S < col_lo + ncx - lo0 ? S : col_lo + ncx - lo0);
         const int lo1 = pp.n_phase > 1 ? pp.phase_lo[1] : (1 << 30);
-        for (int cc = glane; cc < ncx; cc += FG) {
-          int m = (col_lo + cc) % M; if (m < 0) m += M;
+        // (warp-uniform trip count: the TMEM stores are warp-collective)
+        for (int cc0 = 0; cc0 < ncx; cc0 += FG) {
+          const int cc = cc0 + glane;
+          const bool ok = cc < ncx;
+          int m = (col_lo + (ok ? cc : 0)) % M; if (m < 0) m += M;
           int mm = M - m; if (mm == M) mm = 0;
           T2 zm = res[MC > 0 ? padi(m) : m], zc = res[MC > 0 ? padi(mm) : mm];
           zc.y = -zc.y;                                              // conj Z(-m)
@@ -190,11 +224,16 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           const T2 dd = csub(zm, zc);
           const T2 xb = {T(0.5) * dd.y, T(-0.5) * dd.x};             // (Z(m) - conj Z(-m)) / (2i)
           const int m2 = col_lo + cc;
-          if (MC == 0 || m2 >= lo1) {
+          if (use_tmem) {
+            const int gi = cc0 / 32 - pp.tmem_g0;
+            if (gi >= 0 && gi < pp.tmem_ng)
+              tm_st4(tmem_mine + uint32_t(((pr >> 4) * pp.tmem_ng + gi) * 4), float(xa.x), float(xa.y), float(xb.x),
+                     float(xb.y));
+          } else if (ok && (MC == 0 || m2 >= lo1)) {
             X[(int64_t)a0 * ncx + cc] = xa;
             if (has1) X[(int64_t)a1 * ncx + cc] = xb;
           }
-          if (MC > 0 && m2 < hi0) {
+          if (ok && MC > 0 && m2 < hi0) {
             region[(size_t)a0 * S + (m2 - lo0)] = xa;
             if (has1) region[(size_t)a1 * S + (m2 - lo0)] = xb;
           }
@@ -202,6 +241,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         gsync<FG>(gbar);
       }
     }
+    if (use_tmem) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     __syncthreads();
     PROF_MARK(0);
 
@@ -211,7 +251,20 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       const int lo = pp.phase_lo[ph];
       int ncols = col_lo + ncx - lo; if (ncols > S) ncols = S;
       T2* Gc = region;
-      if (MC == 0 || ph > 0) {                      // pow2 phase 0 was written by the row pass directly
+      if (use_tmem && ph == 1) {                    // phase 1 from TMEM: each warp reads back its own row pairs
+        for (int pr = warp; pr < (L + 1) / 2; pr += 16) {
+          const int a0 = 2 * pr, a1 = a0 + 1;
+          for (int gi = 0; gi < pp.tmem_ng; ++gi) {
+            const float4 v = tm_ld4(tmem_mine + uint32_t(((pr >> 4) * pp.tmem_ng + gi) * 4));
+            const int m2 = col_lo + 32 * (pp.tmem_g0 + gi) + lane;
+            if (m2 >= lo && m2 < lo + ncols && m2 - col_lo < ncx) {
+              Gc[(size_t)a0 * S + (m2 - lo)] = T2{v.x, v.y};
+              if (a1 < L) Gc[(size_t)a1 * S + (m2 - lo)] = T2{v.z, v.w};
+            }
+          }
+        }
+        __syncthreads();
+      } else if (MC == 0 || ph > 0) {               // pow2 phase 0 was written by the row pass directly
         for (int a = warp; a < L; a += nwarps) {
           const T2* src = X + (int64_t)a * ncx + (lo - col_lo);
           T2* dst = Gc + (size_t)a * S;
@@ -654,6 +707,11 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
     }
   }
   PROF_STORE();
+  if (use_tmem) {
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem_base));
+  }
 }
 
 template <typename T, int W, int MC>

@@ -486,6 +486,16 @@ fbspca_status build_host_plan(Plan& P) {
     ++np;
   }
   pp.n_phase = np;
+  // TMEM parking of the second phase's columns (kernels_polar.cu): M = 256 compile-time kernel with 16 FFT warps and two
+  // phases; the warp's four row pairs x ng 32-column groups x 4 floats fit 64 TMEM columns (4 warps per lane quarter)
+  pp.tmem_x = 0;
+  if (M == 256 && P.n_theta == 2 * M && P.dt == FBSPCA_F32 && w == 6 && pp.fft_warps == 16 && np == 2 &&
+      (L + 1) / 2 <= 4 * 16 && !getenv("FBSPCA_NO_TMEM_X")) {
+    const int c1 = pp.phase_lo[1] - pp.col_lo;               // first row-pass column index of phase 1
+    pp.tmem_g0 = c1 / 32;
+    pp.tmem_ng = (pp.ncols_x - 1) / 32 - pp.tmem_g0 + 1;
+    if (pp.tmem_ng >= 1 && pp.tmem_ng <= 4) pp.tmem_x = 1;
+  }
   pp.phase_node_begin[np] = int(P.nodes.size());
   pp.phase_dbl_begin[np] = int(P.dnoderec.size() / 8);
   pp.phase_quad_begin[np] = int(P.qnoderec.size() / 12);
