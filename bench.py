@@ -128,33 +128,27 @@ PAPER_IMG_S = {"T3": (1e5 / (1438.0 + 42.0), "P:490-492: 1,438 s expansion + 42 
 
 
 def cpu_baseline(cfg, seconds_target=15.0):
-    """The oracle as it stands (expansion + covariance) on a bounded sample of the same workload."""
+    """The oracle as it stands (expansion + covariance) on a bounded sample of the same workload: the sample grows
+    until it takes about seconds_target of host time (at most 1,024 images, three sizings)."""
     import numpy as np
     import oracle as O
     import synth
+    import torch
     basis = O.build_basis(cfg["c"], cfg["R"])
     sig = synth.blobs.noise_sigma(cfg)
-    imgs = synth.blob_images(cfg, 0, 2, sigma_n=sig).double().numpy()
-    O.block_covariance(O.expand(imgs[:1], basis))          # first-call costs out of the per-image estimate
-    t0 = time.perf_counter()
-    O.block_covariance(O.expand(imgs, basis))
-    per = (time.perf_counter() - t0) / 2
-    m = max(2, min(512, int(seconds_target / max(per, 1e-3))))
-    imgs = synth.blob_images(cfg, 0, m, sigma_n=sig).double().numpy()
-    t0 = time.perf_counter()
-    O.block_covariance(O.expand(imgs, basis))
-    dt = time.perf_counter() - t0
-    if dt < 0.5 * seconds_target and m < 512:    # the 2-image probe carries per-call costs: size once more
-        m = max(m + 1, min(512, int(m * seconds_target / dt)))
+    m, dt = 32, 0.0
+    for _ in range(3):
         imgs = synth.blob_images(cfg, 0, m, sigma_n=sig).double().numpy()
         t0 = time.perf_counter()
         O.block_covariance(O.expand(imgs, basis))
         dt = time.perf_counter() - t0
-    import torch
+        if dt >= 0.5 * seconds_target or m >= 1024:
+            break
+        m = max(m + 1, min(1024, int(m * seconds_target / max(dt, 1e-3))))
     return {"value": m / dt, "unit": "images/s", "cores": torch.get_num_threads(), "host_cpus": os.cpu_count(),
             "kind": "oracle",
             "sample": f"first {m} images of {cfg['name']} (oracle: direct Fourier sum + FFT + GL + fp64 covariance), "
-                      f"{dt:.1f} s on the host, numpy/BLAS threads = all cores"}
+                      f"{dt:.1f} s on the host, torch/BLAS threads = all cores"}
 
 
 def _threads():
