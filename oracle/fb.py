@@ -170,9 +170,13 @@ def polar_ft_direct(images: np.ndarray, basis: Basis, chunk: int | None = None,
         E1 = torch.exp(-2j * math.pi * torch.outer(k1[s:s + node_chunk], idx))   # (nodes, L): e^{-2pi i xi1 i1}
         E2 = torch.exp(-2j * math.pi * torch.outer(k2[s:s + node_chunk], idx))   # (nodes, L): e^{-2pi i xi2 i2}
         if dense:
-            K = (E1[:, :, None] * E2[:, None, :]).reshape(-1, L * L)           # K[node, i1 L + i2]
+            # K[node, i1 L + i2] = E1[node, i1] E2[node, i2], real and imaginary parts written out:
+            #   Re K = Re E1 Re E2 - Im E1 Im E2,   Im K = Re E1 Im E2 + Im E1 Re E2   (batched outer products)
+            e1r, e1i, e2r, e2i = E1.real, E1.imag, E2.real, E2.imag
+            Kr = torch.bmm(torch.stack([e1r, -e1i], -1), torch.stack([e2r, e2i], 1)).reshape(-1, L * L)
+            Ki = torch.bmm(torch.stack([e1r, e1i], -1), torch.stack([e2i, e2r], 1)).reshape(-1, L * L)
             If = I3.reshape(n, L * L)
-            Fh[:, s:s + node_chunk] = torch.complex(If @ K.real.contiguous().T, If @ K.imag.contiguous().T)
+            Fh[:, s:s + node_chunk] = torch.complex(If @ Kr.T, If @ Ki.T)
         else:
             for b in range(n):
                 T = torch.complex(I3[b] @ E2.real.T.contiguous(), I3[b] @ E2.imag.T.contiguous())  # (i1, node)
