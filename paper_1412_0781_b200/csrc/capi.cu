@@ -229,6 +229,10 @@ fbspca_status upload_plan(Plan& P) {
   const int64_t ncoef = P.coef_off[nk];
   if (f32) {
     auto tab = cast_vec<float>(P.table);
+    // rings sampled at every s_j-th angle (plan.cpp): the angular quadrature weight 2 pi / (n_theta / s_j) is the
+    // table's 2 pi / n_theta times s_j, a power of two -- folded in exactly here (K4's fp32 tables only)
+    for (int64_t row = 0; row < ncoef; ++row)
+      for (int j = 0; j < P.n_xi; ++j) tab[row * P.n_xi + j] *= float(P.ring_s[j]);
     FB_CUDA(upload(&P.d_table, tab.data(), tab.size()), "upload table");
     std::vector<float> hi(tab.size()), lo(tab.size());
     for (size_t i = 0; i < tab.size(); ++i) {          // tf32 round-to-nearest (ties away), as cvt.rna.tf32
@@ -261,6 +265,7 @@ fbspca_status upload_plan(Plan& P) {
   FB_CUDA(upload((void**)&P.d_cs, P.cs.data(), P.cs.size()), "upload cs");
   FB_CUDA(upload((void**)&P.d_nodes, P.nodes.data(), P.nodes.size()), "upload nodes");
   FB_CUDA(upload((void**)&P.d_kj0, P.kj0.data(), P.kj0.size()), "upload kj0");
+  FB_CUDA(upload((void**)&P.d_ring_s, P.ring_s.data(), P.ring_s.size()), "upload ring strides");
   FB_CUDA(upload((void**)&P.d_noderec, P.noderec.data(), P.noderec.size()), "upload node records");
   FB_CUDA(upload((void**)&P.d_dnoderec, P.dnoderec.data(), P.dnoderec.size()), "upload double node records");
   FB_CUDA(upload((void**)&P.d_qnoderec, P.qnoderec.data(), P.qnoderec.size()), "upload quad node records");
@@ -287,7 +292,7 @@ fbspca_status upload_plan(Plan& P) {
   FB_CUDA(cudaMalloc((void**)&P.d_eig_sweeps, nk * sizeof(int)), "alloc eig sweeps");
   (void)ncoef;
   pp.deapod = P.d_deapod; pp.tw_M = P.d_tw_M; pp.tw_theta = P.d_tw_theta;
-  pp.rho = P.d_rho; pp.cs = P.d_cs; pp.nodes = P.d_nodes; pp.kj0 = P.d_kj0;
+  pp.rho = P.d_rho; pp.cs = P.d_cs; pp.nodes = P.d_nodes; pp.kj0 = P.d_kj0; pp.ring_s = P.d_ring_s;
   pp.noderec = reinterpret_cast<const int4*>(P.d_noderec);
   pp.dnoderec = reinterpret_cast<const int4*>(P.d_dnoderec);
   pp.qnoderec = reinterpret_cast<const int4*>(P.d_qnoderec);
@@ -303,7 +308,7 @@ void free_plan(Plan& P) {
                   P.d_pscratch, P.d_ghat, P.d_partial, P.d_p, P.d_coef_off, P.d_blk_off, P.d_evec_off,
                   P.d_eig_work, P.d_eig_sweeps, P.d_coef_k, P.d_pp, P.d_cov_scratch, P.d_cov_scratch0, P.d_table_hi, P.d_table_lo, P.d_rbasis,
                   P.d_synth_rho, P.d_synth_pidx, P.d_synth_pir, P.d_synth_pcs, P.d_synth_grp,
-                  P.d_noderec, P.d_dnoderec, P.d_kj0, P.d_qnoderec};
+                  P.d_noderec, P.d_dnoderec, P.d_kj0, P.d_qnoderec, P.d_ring_s};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (cudaEvent_t e : P.event_pool) cudaEventDestroy(e);
   P.event_pool.clear();

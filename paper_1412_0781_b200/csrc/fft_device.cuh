@@ -374,6 +374,99 @@ __device__ void fft_rt(const FftPlan& f, Ld ld, St st, T2* A, T2* B, const T2* t
   }
 }
 
+// ---------------------------------------------------------------- 256-point FFT on a half-warp (radix 16 x 16)
+// M = 256 (C3) kernels: each half-warp transforms its own 256-point sequence with 16 values per lane, so a warp
+// runs two FFTs at once.  t = 16 t1 + t2, k = k1 + 16 k2:
+//   X[k1 + 16 k2] = sum_t2 w16^(t2 k2) [ w256^(t2 k1) sum_t1 x[16 t1 + t2] w16^(t1 k1) ]
+// Lane q = t2 does the inner 16-point DFT over t1 in registers, twiddles, and writes row k1 of a 16 x 17 padded
+// transpose buffer; lane q = k1 reads row q back and does the outer DFT over t2.  One shared-memory round trip
+// per point (the Stockham 8-8-4 path: two), no index swizzle arithmetic (the padding keeps both the row writes and
+// the row reads conflict-free: bank pair (k1 + t2) mod 16), and two FFTs per warp instruction stream.
+__host__ __device__ __forceinline__ float2 hadd(float2 a, float2 b) {
+#ifdef __CUDA_ARCH__
+  return padd(a, b);
+#else
+  return {a.x + b.x, a.y + b.y};
+#endif
+}
+__host__ __device__ __forceinline__ float2 hsub(float2 a, float2 b) {
+#ifdef __CUDA_ARCH__
+  return psub(a, b);
+#else
+  return {a.x - b.x, a.y - b.y};
+#endif
+}
+// forward 4-point DFT in place: (a, b, c, d) <- (X0, X1, X2, X3)
+__host__ __device__ __forceinline__ void dft4f(float2& a, float2& b, float2& c, float2& d) {
+  const float2 s0 = hadd(a, c), d0 = hsub(a, c), s1 = hadd(b, d), t = hsub(b, d);
+  const float2 d1 = {t.y, -t.x};                                     // -i (b - d)
+  a = hadd(s0, s1); c = hsub(s0, s1);
+  b = hadd(d0, d1); d = hsub(d0, d1);
+}
+// forward 16-point DFT in place, natural order in and out (4 x 4: t = 4 a + b, k = k0 + 4 k1).
+// HZ: inputs t in [4, 12) are known zeros (zero-padded rows / columns of K1) and are not read.
+template <bool HZ>
+__host__ __device__ __forceinline__ void dft16(float2 (&v)[16]) {
+  constexpr float C = 0.92387953251128675613f, S = 0.38268343236508977173f, H = 0.70710678118654752440f;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    if constexpr (HZ) {            // x[b], x[12 + b] only: Y[k0] = x0 + i^k0 x3
+      const float2 x0 = v[b], x3 = v[12 + b];
+      v[b] = hadd(x0, x3);
+      v[8 + b] = hsub(x0, x3);
+      v[4 + b] = float2{x0.x - x3.y, x0.y + x3.x};
+      v[12 + b] = float2{x0.x + x3.y, x0.y - x3.x};
+    } else {
+      dft4f(v[b], v[4 + b], v[8 + b], v[12 + b]);
+    }
+  }
+  // twiddles w16^(b k0) on v[b + 4 k0]
+  auto mulc = [](float2 x, float wr, float wi) { return float2{x.x * wr - x.y * wi, x.x * wi + x.y * wr}; };
+  v[5] = mulc(v[5], C, -S);                                              // w^1
+  v[9] = float2{(v[9].x + v[9].y) * H, (v[9].y - v[9].x) * H};           // w^2
+  v[13] = mulc(v[13], S, -C);                                            // w^3
+  v[6] = float2{(v[6].x + v[6].y) * H, (v[6].y - v[6].x) * H};           // w^2
+  v[10] = float2{v[10].y, -v[10].x};                                     // w^4 = -i
+  v[14] = float2{(v[14].y - v[14].x) * H, -(v[14].x + v[14].y) * H};     // w^6
+  v[7] = mulc(v[7], S, -C);                                              // w^3
+  v[11] = float2{(v[11].y - v[11].x) * H, -(v[11].x + v[11].y) * H};     // w^6
+  v[15] = mulc(v[15], -C, S);                                            // w^9
+#pragma unroll
+  for (int k0 = 0; k0 < 4; ++k0) dft4f(v[4 * k0], v[4 * k0 + 1], v[4 * k0 + 2], v[4 * k0 + 3]);
+  // v[4 k0 + k1] = X[k0 + 4 k1]  ->  natural order (a compile-time register renaming)
+  float2 o[16];
+#pragma unroll
+  for (int k0 = 0; k0 < 4; ++k0)
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) o[k0 + 4 * k1] = v[4 * k0 + k1];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = o[i];
+}
+__host__ __device__ __forceinline__ constexpr int hw_idx(int k) { return (k >> 4) * 17 + (k & 15); }   // natural order
+
+#ifdef __CUDACC__
+// v[t1] = x[16 t1 + q] in, v[k2] = X[q + 16 k2] out (q = lane & 15).  buf: the half-warp's kHwBuf-element buffer;
+// tw2[k1 * 16 + t2] = w256^(k1 t2).  Warp-collective (both half-warps call it together).
+template <bool HZ>
+__device__ __forceinline__ void fft256_hw(float2 (&v)[16], float2* buf, const float2* __restrict__ tw2, int q) {
+  dft16<HZ>(v);
+#pragma unroll
+  for (int k1 = 1; k1 < 16; ++k1) v[k1] = cmul(v[k1], tw2[k1 * 16 + q]);
+#pragma unroll
+  for (int k1 = 0; k1 < 16; ++k1) buf[k1 * 17 + q] = v[k1];
+  __syncwarp();
+#pragma unroll
+  for (int t2 = 0; t2 < 16; ++t2) v[t2] = buf[q * 17 + t2];
+  __syncwarp();
+  dft16<false>(v);
+}
+// the result in natural order in buf (hw_idx) for readers that need X[k] and X[N - k] together
+__device__ __forceinline__ void hw_store_natural(const float2 (&v)[16], float2* buf, int q) {
+#pragma unroll
+  for (int k2 = 0; k2 < 16; ++k2) buf[k2 * 17 + q] = v[k2];
+}
+#endif
+
 template <typename T2, int NC, bool HZ = false, int GS = 32, class Ld, class St>
 __device__ __forceinline__ void fft_any(const FftPlan& f, Ld ld, St st, T2* A, T2* B, const T2* tw, int lane,
                                         int bar = 0) {

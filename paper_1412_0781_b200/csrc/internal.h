@@ -23,6 +23,11 @@ static_assert(kCovBatchTc / kCovChunkTc <= kCovMaxChunks, "covariance scratch sl
 constexpr int kCovChunk0 = 128;         // images per k = 0 fp64 CTA (tensor-core path: its own scratch, more CTAs)
 constexpr int kCovMaxSub0 = kCovBatchTc / kCovChunk0;
 
+// Per-warp FFT scratch of the polar kernel (complex elements): two ping-pong buffers of M (padded to 16), or for the
+// M = 256 fp32 kernel (hw: half-warp radix-16 x 16 FFTs, fft_device.cuh) two half-warp buffers of 16 rows x 17.
+constexpr int kHwBuf = 272;
+__host__ __device__ constexpr int polar_warp_scratch(int M, bool hw) { return hw ? 2 * kHwBuf : 2 * ((M + 15) & ~15); }
+
 // Stockham radix plan for a length-N FFT (N = prod radices; radices in {2,3,4,5,8}).
 struct FftPlan {
   int n = 0;
@@ -61,6 +66,7 @@ struct PolarParams {
   const double* cs;               // half x 2: cos(theta_l), sin(theta_l)
   const uint32_t* nodes;          // (j << 16) | l, grouped by phase
   const int* kj0;                 // per k: first ring j K4 reads (rings below carry |T_k| < 1e-9 max|T_k|; plan.cpp)
+  const int* ring_s;              // per ring j: angular stride s_j (ring sampled at theta_l, l = 0, s_j, 2 s_j, ..; plan.cpp)
   const int4* noderec;            // per entry {b1 | b2 << 16, t1, t2, (j << 16) | l} (fp32 path)
   const int4* dnoderec;           // per double entry 2 int4 (plan.cpp "Double entries")
   const int4* qnoderec;           // per quad entry 3 int4 (plan.cpp "Quad entries")
@@ -92,6 +98,8 @@ struct Plan {
   std::vector<double> rbasis;            // [coef row][j]: N J_k(R xi_j/c)  (Eq. (sPCArad))
   std::vector<int> kj0;                  // per k: first ring j of K4's sum (multiple of 8; 0 for fp64 plans)
   int* d_kj0 = nullptr;
+  std::vector<int> ring_s;               // per ring j: angular stride s_j (n_theta / s_j samples; 1 = every theta_l)
+  int* d_ring_s = nullptr;
   // NUFFT
   int M = 0, w = 0;
   double beta = 0;
@@ -196,6 +204,6 @@ cudaError_t launch_cov_k0(const Plan& P, const void* d_coeffs, int64_t ld, int64
 int cov_tma_chunk();                    // images per split-K chunk of the tensor-core K5 (a multiple of kCovChunk)
 bool cov_uses_tc(const Plan& P, int64_t ld);   // K5 for k >= 1 on tcgen05 for this plan and leading dimension
 int fft_values_per_lane(const FftPlan& f);
-int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps, int nk);
+int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps, int nk, bool hw);
 
 }  // namespace fbspca

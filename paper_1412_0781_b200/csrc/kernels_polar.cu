@@ -66,6 +66,28 @@ template <> struct Es<float> {
     const float s = sqrt_approx(fmaxf(fmaf(-z, z, 1.f), 0.f));
     return ex2_approx(fmaf(s, bl, -bl));
   }
+  // phi(ta - q), phi(tb - q) with packed f32x2 arithmetic: d = t - q, r = hw^2 - d^2 = (q - t) d + hw^2 (FADD2, FADD2,
+  // FFMA2), e = ex2(bl s / hw - bl), s = sqrt|r| (the |.| only absorbs rounding at |d| = hw; FFMA2), 4 MUFU
+  __device__ __forceinline__ void pair(float ta, float tb, float q, float& pa, float& pb) const {
+    const float hw = 1.f / inv_hw, hw2 = hw * hw, blh = bl * inv_hw;
+    unsigned long long t, qq, d, dn, r, e, c2, h2, b2;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(t) : "f"(ta), "f"(tb));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(qq) : "f"(q));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(h2) : "f"(hw2));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(t), "l"(qq));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dn) : "l"(qq), "l"(t));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(dn), "l"(d), "l"(h2));
+    float ra, rb;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(ra), "=f"(rb) : "l"(r));
+    const float sa = sqrt_approx(fabsf(ra)), sb = sqrt_approx(fabsf(rb));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(e) : "f"(sa), "f"(sb));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c2) : "f"(blh));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(b2) : "f"(-bl));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(e), "l"(c2), "l"(b2));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(ra), "=f"(rb) : "l"(r));
+    pa = ex2_approx(ra);
+    pb = ex2_approx(rb);
+  }
 };
 template <> struct Es<double> {
   double inv_hw, beta;
@@ -115,12 +137,16 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
   T2* wscr = reinterpret_cast<T2*>(base + (((size_t)(M + nt) * sizeof(T2) + (size_t)L * sizeof(T) +
                                             (size_t)(pp.k_max + 1) * sizeof(int) + 15) / 16) * 16);
   const int MP = (M + 15) & ~15, NTP = (nt + 15) & ~15;   // ping-pong lengths: padi permutes within 16-blocks
-  T2* region = wscr + (size_t)pp.fft_warps * 2 * MP;
+  // HW: M = 256 fp32 -- every FFT (rows, columns, rings) is the half-warp radix-16 x 16 fft256_hw, two per warp
+  constexpr bool HW = (MC == 256) && sizeof(T) == 4;
+  static_assert(!HW || W <= 16, "fft256_hw column stores assume PADR <= 16 wrapped rows");
+  const int WS = polar_warp_scratch(M, HW);
+  T2* region = wscr + (size_t)pp.fft_warps * WS;
   // FFT groups: one warp (FG = 32) or, for M = 512 / 600 / 720 (8 ping-pong pairs fit, not 16), a warp pair (FG = 64)
   // on named barrier 1 + grp, so all 16 warps run the row / column / ring FFTs
   constexpr int FG = (MC == 512 || MC == 600 || MC == 720) ? 64 : 32;
   const int grp = warp / (FG / 32), glane = tid & (FG - 1), gbar = 1 + grp;
-  T2* myA = wscr + (size_t)grp * 2 * MP;          // row / column FFT ping-pong
+  T2* myA = wscr + (size_t)grp * WS;             // row / column FFT ping-pong
   T2* myB = myA + MP;
   T2* angA = region + (size_t)warp * 2 * NTP;     // angular FFT ping-pong (region is free then)
   T2* angB = angA + NTP;
@@ -128,7 +154,10 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
     const T2* gtM = reinterpret_cast<const T2*>(pp.tw_M);
     const T2* gtT = reinterpret_cast<const T2*>(pp.tw_theta);
     const T* gd = reinterpret_cast<const T*>(pp.deapod);
-    if constexpr (MC > 0) {
+    if constexpr (HW) {                                          // tw2[k1 16 + t2] = w256^(k1 t2)
+      for (int i = tid; i < 256; i += nthr) twM[i] = gtM[((i >> 4) * (i & 15)) & 255];
+      for (int i = tid; i < NC / 2; i += nthr) twT[i] = gtT[i];
+    } else if constexpr (MC > 0) {
       build_stage_tw<T2, MC>(twM, gtM, tid, nthr);             // per-stage tables (<= M entries)
       for (int i = tid; i < NC / 2; i += nthr) twT[i] = gtT[i];   // ring pairs: e^{-2 pi i t / n_theta}, t < n/2
     } else {
@@ -191,7 +220,72 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       Isrc = simg;
     }
     // ---------------- K1a: row FFTs, two real rows per complex sequence, deapodised + zero-padded on load
-    if (grp < pp.fft_warps) {
+    if constexpr (HW) {
+      // half-warp h of warp w transforms row pair pr = base + h FW + w (FW = fft_warps = 16: the TMEM slot of pr is
+      // pr >> 4 as in the warp-per-pair path), then the whole warp splits and writes both results
+      const int q = lane & 15, h = lane >> 4, FW = pp.fft_warps, nrp = (L + 1) / 2;
+      T2* hb = wscr + (size_t)grp * 2 * kHwBuf;
+      T2* mybuf = hb + h * kHwBuf;
+      const int lo0 = pp.phase_lo[0], hi0 = lo0 + (S < col_lo + ncx - lo0 ? S : col_lo + ncx - lo0);
+      const int lo1 = pp.n_phase > 1 ? pp.phase_lo[1] : (1 << 30);
+      for (int base = 0; grp < FW && base < nrp; base += 2 * FW) {
+        {
+          const int pr = base + h * FW + grp;
+          const bool okp = pr < nrp;
+          const int a0 = okp ? 2 * pr : 0, a1 = a0 + 1;
+          const bool has1 = okp && a1 < L;
+          const T* r0 = Isrc + (int64_t)a0 * L;
+          const T* r1 = Isrc + (int64_t)(has1 ? a1 : a0) * L;
+          const T d0 = okp ? dap[a0] : T(0), d1 = has1 ? dap[a1] : T(0);
+          float2 v[16];
+#pragma unroll
+          for (int t1 = 0; t1 < 16; ++t1) {
+            if (t1 >= 4 && t1 < 12) { v[t1] = float2{0.f, 0.f}; continue; }      // zero padding (HZ)
+            const int t = 16 * t1 + q;
+            const int b = (t < 128 ? t : t - 256) + L / 2;
+            if (b < 0 || b >= L) { v[t1] = float2{0.f, 0.f}; continue; }
+            const T db = dap[b];
+            v[t1] = float2{r0[b] * d0 * db, r1[b] * d1 * db};
+          }
+          fft256_hw<true>(v, mybuf, twM, q);
+          hw_store_natural(v, mybuf, q);
+        }
+        __syncwarp();
+        for (int hh = 0; hh < 2; ++hh) {               // warp-uniform: the TMEM stores are warp-collective
+          const int pr = base + hh * FW + grp;
+          if (pr >= nrp) continue;
+          const T2* res = hb + hh * kHwBuf;
+          const int a0 = 2 * pr, a1 = a0 + 1;
+          const bool has1 = a1 < L;
+          for (int cc0 = 0; cc0 < ncx; cc0 += 32) {
+            const int cc = cc0 + lane;
+            const bool ok = cc < ncx;
+            int m = (col_lo + (ok ? cc : 0)) % M; if (m < 0) m += M;
+            int mm = M - m; if (mm == M) mm = 0;
+            T2 zm = res[hw_idx(m)], zc = res[hw_idx(mm)];
+            zc.y = -zc.y;                                            // conj Z(-m)
+            const T2 xa = {T(0.5) * (zm.x + zc.x), T(0.5) * (zm.y + zc.y)};
+            const T2 dd = csub(zm, zc);
+            const T2 xb = {T(0.5) * dd.y, T(-0.5) * dd.x};           // (Z(m) - conj Z(-m)) / (2i)
+            const int m2 = col_lo + cc;
+            if (use_tmem) {
+              const int gi = cc0 / 32 - pp.tmem_g0;
+              if (gi >= 0 && gi < pp.tmem_ng)
+                tm_st4(tmem_mine + uint32_t(((pr >> 4) * pp.tmem_ng + gi) * 4), float(xa.x), float(xa.y),
+                       float(xb.x), float(xb.y));
+            } else if (ok && m2 >= lo1) {
+              X[(int64_t)a0 * ncx + cc] = xa;
+              if (has1) X[(int64_t)a1 * ncx + cc] = xb;
+            }
+            if (ok && m2 < hi0) {
+              region[(size_t)a0 * S + (m2 - lo0)] = xa;
+              if (has1) region[(size_t)a1 * S + (m2 - lo0)] = xb;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    } else if (grp < pp.fft_warps) {
       for (int pr = grp; pr < (L + 1) / 2; pr += pp.fft_warps) {
         const int a0 = 2 * pr, a1 = a0 + 1;
         const bool has1 = a1 < L;
@@ -278,7 +372,35 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         if (ph == pp.n_phase - 1) l2_discard(X, (size_t)L * ncx * sizeof(T2), tid, nthr);
       }
       PROF_MARK(1);
-      if (grp < pp.fft_warps) {
+      if constexpr (HW) {
+        // half-warp h of warp w: column cc = base + 2 w + h, in place (all inputs are in registers before the first
+        // store: fft256_hw's transpose sync), output fftshifted with PADR wrapped duplicate rows
+        const int q = lane & 15, h = lane >> 4, FW = pp.fft_warps;
+        T2* mybuf = wscr + (size_t)grp * 2 * kHwBuf + h * kHwBuf;
+        for (int base = 0; grp < FW && base + 2 * grp < ncols; base += 2 * FW) {      // warp-uniform bound
+          const int cc = base + 2 * grp + h;
+          const bool okc = cc < ncols;
+          T2* col = Gc + (okc ? cc : 0);
+          float2 v[16];
+#pragma unroll
+          for (int t1 = 0; t1 < 16; ++t1) {
+            if (t1 >= 4 && t1 < 12) { v[t1] = float2{0.f, 0.f}; continue; }
+            const int t = 16 * t1 + q;
+            const int a = (t < 128 ? t : t - 256) + L / 2;
+            v[t1] = (okc && a >= 0 && a < L) ? col[(size_t)a * S] : float2{0.f, 0.f};
+          }
+          fft256_hw<true>(v, mybuf, twM, q);
+          if (okc) {
+#pragma unroll
+            for (int k2 = 0; k2 < 16; ++k2) {
+              const int m1 = k2 < 8 ? q + 16 * k2 : q + 16 * k2 - 256;
+              col[(size_t)(m1 + row0) * S] = v[k2];
+              if (k2 == 8 && m1 < -128 + PADR) col[(size_t)(m1 + 256 + row0) * S] = v[k2];
+              if (k2 == 7 && m1 >= 128 - PADR) col[(size_t)(m1 - 256 + row0) * S] = v[k2];
+            }
+          }
+        }
+      } else if (grp < pp.fft_warps) {
         for (int cc = grp; cc < ncols; cc += pp.fft_warps) {
           T2* col = Gc + cc;
           auto ld = [&](int t) -> T2 {
@@ -372,9 +494,9 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           {
             float wa[6], va[6], wb[6], vb[6];
 #pragma unroll
-            for (int q = 0; q < 6; ++q) {
-              wa[q] = phi(t1a - float(q)); va[q] = phi(t2a - float(q));
-              wb[q] = phi(t1b - float(q)); vb[q] = phi(t2b - float(q));
+            for (int q = 0; q < 6; ++q) {               // nodes a and b in one f32x2 pair per direction
+              phi.pair(t1a, t1b, float(q), wa[q], wb[q]);
+              phi.pair(t2a, t2b, float(q), va[q], vb[q]);
             }
             const bool o1a = of & 1, o2a = of & 2, o1b = of & 4, o2b = of & 8;
 #pragma unroll
@@ -405,11 +527,17 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             aa = rfma(xa[r], sa, aa); ab = rfma(xb[r], sb, ab);
             ma = rfma(xa[r], na, ma); mb = rfma(xb[r], nb2, mb);
           }
-          const int ja = int(uint32_t(r1.x) >> 16), la = r1.x & 0xFFFF;
-          // nodes a, b are (ja, la), (ja, la + 1); their mirrors (ja, half - la), (ja, half - la - 1).  half is even,
-          // so exactly one of the two adjacent pairs starts 16-byte aligned: that one is one 16-byte store
+          const int ja = int(uint32_t(r1.x) >> 16), la = r1.x & 0xFFFF, lb = r1.w & 0xFFFF;
+          // nodes a, b are (ja, la), (ja, lb); their mirrors (ja, half - la), (ja, half - lb).  Adjacent (lb = la + 1,
+          // rings sampled at every angle): half is even, so exactly one of the two adjacent pairs starts 16-byte
+          // aligned and is one 16-byte store.  Strided rings (lb = la + s_j): four 8-byte stores.
           T2* prow = Pol + (int64_t)ja * half;
-          if (la & 1) {
+          if (lb != la + 1) {
+            prow[la] = aa;
+            prow[lb] = ab;
+            prow[half - la] = ma;
+            prow[half - lb] = mb;
+          } else if (la & 1) {
             prow[la] = aa;
             prow[la + 1] = ab;
             *reinterpret_cast<float4*>(prow + (half - la - 1)) = make_float4(mb.x, mb.y, ma.x, ma.y);
@@ -485,28 +613,35 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
     // (or odd) k of a half-warp (k = 2m, m = 0..15) and the write-out's four consecutive k of a half-warp land in
     // distinct 8-byte bank pairs (no 2-way conflicts; GS odd, <= 33 rings per row + 1 spare slot)
     auto sidx = [GS](int k, int jj) { return (size_t)k * GS + jj + ((k >> 4) & 1); };
-    // MC = 256 (one ring pair per warp per group): the pair's first-stage inputs f[lane + 32 r], r < 8, of both
-    // rings are loaded into registers one group ahead (the loads of group j0 + G fly during group j0's FFTs and
-    // write-out), and feed both the U and the V transform -- one L2 read of the polar samples, latency hidden.
-    constexpr bool REGPF = (MC == 256) && sizeof(T) == 4;
-    T2 pfa[REGPF ? 8 : 1], pfb[REGPF ? 8 : 1];
+    // MC = 256 (HW: one ring pair per warp per group): half-warp 0 transforms U = DFT(Re f_j + i Re f_j'), half-warp 1
+    // V = DFT((Im f_j + i Im f_j') w^t) at the same time.  Each lane's 16 inputs f[16 t1 + q] of both rings (its
+    // half's component) are loaded into registers one group ahead (the loads of group j0 + G fly during group j0's
+    // FFTs and write-out) -- one L2 read of the polar samples, latency hidden.
+    constexpr bool REGPF = HW;
+    float pfa[REGPF ? 16 : 1], pfb[REGPF ? 16 : 1];
     const bool regpf = REGPF && G <= 2 * pp.fft_warps;
     auto load_pair = [&](int jg) {
       if constexpr (REGPF) {
         const int jj = 2 * warp, gg = min(G, n_xi - jg);
         if (jg < n_xi && warp < pp.fft_warps && jj < gg) {
-          const T2* fa = Pol + (int64_t)(jg + jj) * half;
+          const float* fa = reinterpret_cast<const float*>(Pol + (int64_t)(jg + jj) * half) + (lane >> 4);
           const bool two = jj + 1 < gg;
+          const float* fb = two ? fa + 2 * half : fa;
+          const int q = lane & 15;
+          // ring j sampled at every s_j-th angle (plan.cpp): the unsampled positions of the half ring are zeros of
+          // the stuffed sequence, never written by the gather and not loaded here
+          const int ma = __ldg(pp.ring_s + jg + jj) - 1, mb = two ? __ldg(pp.ring_s + jg + jj + 1) - 1 : 0;
           // volatile: issued here (not sunk to the use a group later), completion tracked by the scoreboard
-          const T2* fb = two ? fa + half : fa;
 #pragma unroll
-          for (int r = 0; r < 8; ++r) {
-            asm volatile("ld.global.v2.f32 {%0, %1}, [%2];" : "=f"(pfa[r].x), "=f"(pfa[r].y) : "l"(fa + lane + 32 * r));
-            asm volatile("ld.global.v2.f32 {%0, %1}, [%2];" : "=f"(pfb[r].x), "=f"(pfb[r].y) : "l"(fb + lane + 32 * r));
-          }
-          if (!two) {
-#pragma unroll
-            for (int r = 0; r < 8; ++r) pfb[r] = T2{T(0), T(0)};
+          for (int t1 = 0; t1 < 16; ++t1) {
+            const int t = 16 * t1 + q;
+            pfa[t1] = 0.f;
+            pfb[t1] = 0.f;
+            // predicated loads (no branches): @p ld, the register keeps its 0 otherwise
+            asm volatile("{ .reg .pred p; setp.eq.s32 p, %2, 0; @p ld.global.f32 %0, [%1]; }"
+                         : "+f"(pfa[t1]) : "l"(fa + 2 * t), "r"(t & ma));
+            asm volatile("{ .reg .pred p; setp.eq.s32 p, %2, 0; @p ld.global.f32 %0, [%1]; }"
+                         : "+f"(pfb[t1]) : "l"(fb + 2 * t), "r"(two ? (t & mb) : 1));
           }
         }
       }
@@ -518,45 +653,32 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       if constexpr (REGPF) if (regpf) {
         done_reg = true;
         const int kmx = pp.k_max;
-        T2* res = fft_result_in_A<MC>() ? myA : myB;
-        auto stR = [res](int i, T2 v) { res[padi(i)] = v; };
-        const int jj = 2 * warp;
+        const int jj = 2 * warp, q = lane & 15, h = lane >> 4;
+        T2* mybuf = wscr + (size_t)warp * 2 * kHwBuf + h * kHwBuf;
         if (warp < pp.fft_warps && jj < g) {
           const bool two = jj + 1 < g;
-          T2 ca[REGPF ? 8 : 1], cb[REGPF ? 8 : 1];
+          float2 v[16];
 #pragma unroll
-          for (int r = 0; r < (REGPF ? 8 : 1); ++r) { ca[r] = pfa[r]; cb[r] = pfb[r]; }
+          for (int t1 = 0; t1 < 16; ++t1) {             // V (h = 1): times w^t; U: times 1 (selects, no branch)
+            const T2 tw = twT[16 * t1 + q];
+            v[t1] = cmul(float2{pfa[t1], pfb[t1]}, float2{h ? tw.x : 1.f, h ? tw.y : 0.f});
+          }
           load_pair(j0 + G);                          // next group's inputs, consumed one iteration later
-          // stage-1 index t = lane + 32 r  ->  r = (t - lane) >> 5 (compile-time after unrolling)
-          auto ldu = [&](int t) -> T2 { const int r = (t - lane) >> 5; return T2{ca[r].x, cb[r].x}; };
-          fft_ct<T2, MC>(ldu, stR, myA, myB, twM, lane);
+          fft256_hw<false>(v, mybuf, twM, q);
+          hw_store_natural(v, mybuf, q);
           __syncwarp();
-          for (int m = lane; 2 * m <= kmx; m += 32) {
-            const T2 u = res[padi(m)];
-            T2 uc = res[padi(m == 0 ? 0 : MC - m)];
+          // even k = 2m from U (h = 0): ghat_j = U(m) + conj U(-m), ghat_j' = -i (U(m) - conj U(-m));
+          // odd k = 2m + 1 from V (h = 1): ghat_j = i (V(m) + conj V(N-1-m)), ghat_j' = V(m) - conj V(N-1-m)
+          for (int m = q; 2 * m + h <= kmx; m += 16) {
+            const T2 u = mybuf[hw_idx(m)];
+            T2 uc = mybuf[hw_idx((256 - m - h) & 255)];
             uc.y = -uc.y;
             const T2 sp = cadd(u, uc), dm = csub(u, uc);
-            stg[sidx(2 * m, jj)] = sp;
-            if (two) stg[sidx(2 * m, jj + 1)] = T2{dm.y, -dm.x};
+            stg[sidx(2 * m + h, jj)] = h ? T2{-sp.y, sp.x} : sp;
+            if (two) stg[sidx(2 * m + h, jj + 1)] = h ? dm : T2{dm.y, -dm.x};
           }
           __syncwarp();
           PROF_MARK(6);
-          auto ldv = [&](int t) -> T2 {
-            const int r = (t - lane) >> 5;
-            return cmul(T2{ca[r].y, cb[r].y}, twT[t]);
-          };
-          fft_ct<T2, MC>(ldv, stR, myA, myB, twM, lane);
-          __syncwarp();
-          for (int m = lane; 2 * m + 1 <= kmx; m += 32) {
-            const T2 v = res[padi(m)];
-            T2 vc = res[padi(MC - 1 - m)];
-            vc.y = -vc.y;
-            const T2 sp = cadd(v, vc), dm = csub(v, vc);
-            stg[sidx(2 * m + 1, jj)] = T2{-sp.y, sp.x};
-            if (two) stg[sidx(2 * m + 1, jj + 1)] = dm;
-          }
-          __syncwarp();
-          PROF_MARK(7);
         }
       }
       if (done_reg) {
@@ -777,10 +899,10 @@ extern "C" int fbspca_debug_phase_prof(unsigned long long* out, int n) {
 }
 #endif
 
-int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps, int nk) {
+int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps, int nk, bool hw) {
   return (int)(((sizeof(PolarParams) + 15) / 16) * 16) +
          (int)((((M + n_theta) * csz + L * (csz / 2) + nk * (int)sizeof(int)) + 15) / 16) * 16 +
-         nwarps * 2 * ((M + 15) & ~15) * csz;
+         nwarps * polar_warp_scratch(M, hw) * csz;
 }
 
 cudaError_t launch_polar(const Plan& P, const void* d_images, int64_t n_img, int64_t stride, cudaStream_t s) {

@@ -317,7 +317,11 @@ fbspca_status build_host_plan(Plan& P) {
   const int fft_share = (P.n_theta == 2 * M) ? 2 : 3;
   while (pp.fft_warps > 2 && pp.fft_warps * 2 * M * csz > cap / fft_share) pp.fft_warps /= 2;
   if (const char* e = getenv("FBSPCA_FFT_WARPS")) pp.fft_warps = std::max(1, std::min(16, atoi(e)));
-  const int fixed = polar_fixed_smem(M, P.n_theta, L, csz, pp.fft_warps, P.k_max + 1);
+  // the compile-time M = 256 fp32 kernel runs every FFT as half-warp radix-16 x 16 transforms (two per warp) with
+  // its own per-warp scratch, on all 16 warps (one ring pair per warp per 32-ring group)
+  const bool hw16 = P.dt == FBSPCA_F32 && w == 6 && M == 256 && P.n_theta == 2 * M;
+  if (hw16) pp.fft_warps = 16;
+  const int fixed = polar_fixed_smem(M, P.n_theta, L, csz, pp.fft_warps, P.k_max + 1, hw16);
   const int budget = cap - fixed;
   const int kk = (P.k_max + 1) | 1;                    // staging row stride (odd)
   const int ntp = (P.n_theta + 15) & ~15;               // ping-pong length (swizzle permutes 16-blocks)
@@ -349,6 +353,7 @@ fbspca_status build_host_plan(Plan& P) {
   }
   const int G = Gsel;
   pp.ring_group = G;
+  if (hw16 && G > 2 * pp.fft_warps) { set_error("internal: M = 256 ring groups exceed one ring pair per warp"); return FBSPCA_ERR_CONFIG; }
   const int region = std::max(std::max(rows_g * S * csz, pp.fft_warps * M * csz),
                               (ring_pairs ? 0 : ang_scr) + ((G + 1) | 1) * kk * csz);
   pp.smem_region_bytes = region;
@@ -389,12 +394,38 @@ fbspca_status build_host_plan(Plan& P) {
   // whose four anchors differ by at most 1 in each direction share one (w + 1) x (w + 1) window: 49 grid loads for
   // the four direct nodes and 49 for their four mirrors -- half the loads per node of a double entry.  Formed
   // greedily over ring pairs (j even) before the doubles; their leaders are skipped below.
+  // Angular stride per ring (M = 256 fp32 kernel).  Ring j only feeds K4 blocks k <= kneed(j) = max{k : kj0[k] <= j},
+  // and F restricted to the ring has no angular content beyond kc(j): by Jacobi-Anger its k-th angular Fourier
+  // coefficient is sum_x I(x) (-i)^k J_k(2 pi xi_j |x|) e^{-i k phi_x}, and |J_k(z)| < 1e-10 for k >= kc(z) past the
+  // turning point, with |x| <= r_c = sqrt(2) ceil(L/2) over the square (no disk mask, reading Q7).  Sampling the ring
+  // at n_theta / s_j angles theta_{l s_j} keeps every needed k free of aliases as long as n_theta / s_j >= kneed + kc
+  // (the nearest alias of k <= kneed is k - n_theta / s_j).  The ring FFT runs on the zero-stuffed ring (the
+  // n_theta-point DFT of the stuffed sequence IS the (n_theta / s_j)-point DFT, exactly), and the quadrature weight
+  // 2 pi s_j / n_theta is the table's 2 pi / n_theta times the power of two s_j (capi.cu upload).  Inner rings need
+  // far fewer angles: C3 gathers 0.70 of the nodes.  FBSPCA_NO_RING_STRIDE=1 samples every ring at all n_theta angles.
+  P.ring_s.assign(P.n_xi, 1);
+  if (hw16 && !getenv("FBSPCA_NO_RING_STRIDE")) {
+    const double rc = std::sqrt(2.0) * std::ceil(0.5 * L);
+    for (int j = 0; j < P.n_xi; ++j) {
+      int kneed = 0;
+      for (int k = 0; k < nk; ++k)
+        if (P.kj0[k] <= j) kneed = k;
+      const double z = 2 * M_PI * P.xi[j] * rc;
+      int kc = int(std::floor(z));
+      while (std::fabs(bessel_j(kc, z)) > 1e-10 || std::fabs(bessel_j(kc + 1, z)) > 1e-10) ++kc;
+      const int need = kneed + kc + 1;
+      int sj = 1;
+      while (sj < 8 && P.n_theta / (2 * sj) >= need && half % (2 * sj) == 0) sj *= 2;
+      P.ring_s[j] = sj;
+    }
+  }
   std::vector<std::array<uint32_t, 1>> quad;                 // (j << 16) | l of the first leader
   std::vector<char> in_quad(size_t(P.n_xi) * (half + 1), 0);
   // measured on B200 (C3): quads cut the gather's shared wavefronts 12 % but ran 2-4 % slower (more registers: spills in
   // the ring pass, more bank conflicts among the fewer doubles) -- kept behind FBSPCA_QUADS=1 for experiments
   // (the kernel's quad loop is compiled only with -DFBSPCA_QUAD_GATHER)
-  const bool quads = doubles && getenv("FBSPCA_QUADS") && atoi(getenv("FBSPCA_QUADS")) == 1;
+  const bool quads = doubles && getenv("FBSPCA_QUADS") && atoi(getenv("FBSPCA_QUADS")) == 1 &&
+                     *std::max_element(P.ring_s.begin(), P.ring_s.end()) == 1;
   if (quads)
     for (int j = 0; j + 1 < P.n_xi; j += 2)
       for (int l = 1; 2 * (l + 1) < half;) {
@@ -413,17 +444,18 @@ fbspca_status build_host_plan(Plan& P) {
         }
       }
   for (int j = 0; j < P.n_xi; ++j) {
-    for (int l = 0; 2 * l <= half; ++l) {
+    const int sj = P.ring_s[j];               // ring j's angles theta_l, l = 0, sj, 2 sj, .. (sj | half/2)
+    for (int l = 0; 2 * l <= half; l += sj) {
       if (in_quad[size_t(j) * (half + 1) + l]) continue;
       const auto a = anchor(j, l);
-      if (doubles && l >= 1 && 2 * (l + 1) < half && !in_quad[size_t(j) * (half + 1) + l + 1]) {
-        const auto b = anchor(j, l + 1);
+      if (doubles && l >= 1 && 2 * (l + sj) < half && !in_quad[size_t(j) * (half + 1) + l + sj]) {
+        const auto b = anchor(j, l + sj);
         const int u1 = std::min(a.first, b.first), u2 = std::min(a.second, b.second);
         const int p = phase_of_double(u2);
         if (std::abs(a.first - b.first) <= 1 && std::abs(a.second - b.second) <= 1 && p >= 0) {
           ph_double[p].push_back({u1, u2, int(dbl.size())});
-          dbl.push_back({(uint32_t(j) << 16) | uint32_t(l), (uint32_t(j) << 16) | uint32_t(l + 1)});
-          ++l;
+          dbl.push_back({(uint32_t(j) << 16) | uint32_t(l), (uint32_t(j) << 16) | uint32_t(l + sj)});
+          l += sj;
           continue;
         }
       }
