@@ -444,14 +444,29 @@ __host__ __device__ __forceinline__ void dft16(float2 (&v)[16]) {
 }
 __host__ __device__ __forceinline__ constexpr int hw_idx(int k) { return (k >> 4) * 17 + (k & 15); }   // natural order
 
+#ifndef FBSPCA_HW_TW_VOLATILE
+#define FBSPCA_HW_TW_VOLATILE 1
+#endif
 #ifdef __CUDACC__
 // v[t1] = x[16 t1 + q] in, v[k2] = X[q + 16 k2] out (q = lane & 15).  buf: the half-warp's kHwBuf-element buffer;
 // tw2[k1 * 16 + t2] = w256^(k1 t2).  Warp-collective (both half-warps call it together).
 template <bool HZ>
 __device__ __forceinline__ void fft256_hw(float2 (&v)[16], float2* buf, const float2* __restrict__ tw2, int q) {
   dft16<HZ>(v);
+  // volatile shared loads: the twiddles depend only on the lane, and hoisting them out of the callers' loops would
+  // pin 30 registers across whole passes (spills in the 128-register kernel)
+#if FBSPCA_HW_TW_VOLATILE
+  const uint32_t twa = static_cast<uint32_t>(__cvta_generic_to_shared(tw2 + q));
+#pragma unroll
+  for (int k1 = 1; k1 < 16; ++k1) {
+    float2 w;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(w.x), "=f"(w.y) : "r"(twa + k1 * 16 * 8));
+    v[k1] = cmul(v[k1], w);
+  }
+#else
 #pragma unroll
   for (int k1 = 1; k1 < 16; ++k1) v[k1] = cmul(v[k1], tw2[k1 * 16 + q]);
+#endif
 #pragma unroll
   for (int k1 = 0; k1 < 16; ++k1) buf[k1 * 17 + q] = v[k1];
   __syncwarp();

@@ -26,6 +26,13 @@ constexpr int kCovMaxSub0 = kCovBatchTc / kCovChunk0;
 // Per-warp FFT scratch of the polar kernel (complex elements): two ping-pong buffers of M (padded to 16), or for the
 // M = 256 fp32 kernel (hw: half-warp radix-16 x 16 FFTs, fft_device.cuh) two half-warp buffers of 16 rows x 17.
 constexpr int kHwBuf = 272;
+// Quad gather entries (M = 256 fp32 kernel, plan.cpp): four pair leaders share one kQuadW x kQuadW window
+// (anchors within kQuadW - 6 of each other; 7: no padded taps, 8: more leaders grouped, 1/3 more taps and weights).
+// Measured on B200 (C3 polar, same box A/B): none 45.98 ms, 7 x 7 49.2 ms, 8 x 8 52.2 ms -- off (0) by default.
+#ifndef FBSPCA_QUAD_W
+#define FBSPCA_QUAD_W 0
+#endif
+constexpr int kQuadW = FBSPCA_QUAD_W;
 __host__ __device__ constexpr int polar_warp_scratch(int M, bool hw) { return hw ? 2 * kHwBuf : 2 * ((M + 15) & ~15); }
 
 // Stockham radix plan for a length-N FFT (N = prod radices; radices in {2,3,4,5,8}).

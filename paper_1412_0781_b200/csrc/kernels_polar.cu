@@ -66,6 +66,28 @@ template <> struct Es<float> {
     const float s = sqrt_approx(fmaxf(fmaf(-z, z, 1.f), 0.f));
     return ex2_approx(fmaf(s, bl, -bl));
   }
+  // phi(ta - q), phi(tb - q), exactly 0 outside the support |d| < hw (quad windows: 8 positions, 6 taps per node)
+  __device__ __forceinline__ void pair_masked(float ta, float tb, float q, float& pa, float& pb) const {
+    const float hw = 1.f / inv_hw, hw2 = hw * hw, blh = bl * inv_hw;
+    unsigned long long t, qq, d, dn, r, e, c2, h2, b2;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(t) : "f"(ta), "f"(tb));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(qq) : "f"(q));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(h2) : "f"(hw2));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(t), "l"(qq));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dn) : "l"(qq), "l"(t));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(dn), "l"(d), "l"(h2));
+    float ra, rb;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(ra), "=f"(rb) : "l"(r));
+    const bool ina = ra > 0.f, inb = rb > 0.f;
+    const float sa = sqrt_approx(fabsf(ra)), sb = sqrt_approx(fabsf(rb));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(e) : "f"(sa), "f"(sb));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c2) : "f"(blh));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(b2) : "f"(-bl));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(e), "l"(c2), "l"(b2));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(ra), "=f"(rb) : "l"(r));
+    pa = ina ? ex2_approx(ra) : 0.f;
+    pb = inb ? ex2_approx(rb) : 0.f;
+  }
   // phi(ta - q), phi(tb - q) with packed f32x2 arithmetic: d = t - q, r = hw^2 - d^2 = (q - t) d + hw^2 (FADD2, FADD2,
   // FFMA2), e = ex2(bl s / hw - bl), s = sqrt|r| (the |.| only absorbs rounding at |d| = hw; FFMA2), 4 MUFU
   __device__ __forceinline__ void pair(float ta, float tb, float q, float& pa, float& pb) const {
@@ -419,66 +441,71 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       __syncthreads();
       PROF_MARK(2);
       if constexpr (sizeof(T) == 4 && W == 6 && MC > 0) {
-#ifdef FBSPCA_QUAD_GATHER   // measured slower on B200; the plan emits quads only with FBSPCA_QUADS=1
-        // quad entries: leaders a = (j, l), b = (j, l + 1), c = (j + 1, l), d = (j + 1, l + 1) over one shared 7 x 7
-        // window at U, first the four direct nodes (rows U1 + r), then their four mirrors (rows -U1 - r): 49 grid
-        // loads per four nodes (plan.cpp "Quad entries")
-        {
+        if constexpr (HW && kQuadW > 0) {
+          // quad entries (plan.cpp): leaders a = (j, l), b = (j, l + s), c = (j + 1, l), d = (j + 1, l + s) over one
+          // shared QW x QW window at U (QW = kQuadW); per window row, the direct row U1 + r and the mirrored row
+          // -U1 - r are loaded once (2 QW grid loads) for all eight nodes.  Column weights y (4 nodes x QW positions)
+          // are held, row weights are evaluated per row; positions outside a node's 6 x 6 support get exactly 0.
+          constexpr int QW = kQuadW;
           const int qb = pp.phase_quad_begin[ph], qe = pp.phase_quad_begin[ph + 1];
+          int4 q0 = make_int4(0, 0, 0, 0), q1 = q0, q2 = q0;     // records one iteration ahead
+          if (qb + tid < qe) {
+            q0 = __ldg(pp.qnoderec + 3 * (qb + tid)); q1 = __ldg(pp.qnoderec + 3 * (qb + tid) + 1);
+            q2 = __ldg(pp.qnoderec + 3 * (qb + tid) + 2);
+          }
           for (int t = qb + tid; t < qe; t += nthr) {
-            const int4 r0 = __ldg(pp.qnoderec + 3 * t), r1 = __ldg(pp.qnoderec + 3 * t + 1), r2 = __ldg(pp.qnoderec + 3 * t + 2);
-            const int u1 = int(short(r0.x & 0xFFFF)), u2 = r0.x >> 16, of = r0.y;
+            const int4 r0 = q0, r1 = q1, r2 = q2;
+            if (t + nthr < qe) {
+              q0 = __ldg(pp.qnoderec + 3 * (t + nthr)); q1 = __ldg(pp.qnoderec + 3 * (t + nthr) + 1);
+              q2 = __ldg(pp.qnoderec + 3 * (t + nthr) + 2);
+            }
+            const int u1 = int(short(r0.x & 0xFFFF)), u2 = r0.x >> 16, sq = r0.y >> 16;
             const int jq = int(uint32_t(r0.z) >> 16), lq = r0.z & 0xFFFF;
-            const float tq[8] = {__int_as_float(r1.x), __int_as_float(r1.y), __int_as_float(r1.z), __int_as_float(r1.w),
-                                 __int_as_float(r2.x), __int_as_float(r2.y), __int_as_float(r2.z), __int_as_float(r2.w)};
-            float xq[4][7], yq[4][7];
+            const float t1[4] = {__int_as_float(r1.x), __int_as_float(r1.y), __int_as_float(r1.z), __int_as_float(r1.w)};
+            const float t2[4] = {__int_as_float(r2.x), __int_as_float(r2.y), __int_as_float(r2.z), __int_as_float(r2.w)};
+            float y[4][QW];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              float wq[6], vq[6];
-#pragma unroll
-              for (int q = 0; q < 6; ++q) { wq[q] = phi(tq[2 * i] - float(q)); vq[q] = phi(tq[2 * i + 1] - float(q)); }
-              const bool o1 = (of >> (2 * i)) & 1, o2 = (of >> (2 * i + 1)) & 1;
-#pragma unroll
-              for (int r = 0; r < 7; ++r) {
-                xq[i][r] = o1 ? (r ? wq[r - 1] : 0.f) : (r < 6 ? wq[r] : 0.f);
-                yq[i][r] = o2 ? (r ? vq[r - 1] : 0.f) : (r < 6 ? vq[r] : 0.f);
-              }
+            for (int c = 0; c < QW; ++c) {
+              phi.pair_masked(t2[0], t2[1], float(c), y[0][c], y[1][c]);
+              phi.pair_masked(t2[2], t2[3], float(c), y[2][c], y[3][c]);
             }
             const T2* gcol = Gc + (u2 - lo);
+            T2 ad[4], am[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { ad[i] = T2{0.f, 0.f}; am[i] = ad[i]; }
 #pragma unroll 1
-            for (int mir = 0; mir < 2; ++mir) {
-              T2 acc[4];
+            for (int r = 0; r < QW; ++r) {
+              float x[4];
+              phi.pair_masked(t1[0], t1[1], float(r), x[0], x[1]);
+              phi.pair_masked(t1[2], t1[3], float(r), x[2], x[3]);
+              const T2* gd = gcol + (size_t)(u1 + r + row0) * S;
+              const T2* gm = gcol + (size_t)(row0 - u1 - r) * S;
+              T2 g[QW];
 #pragma unroll
-              for (int i = 0; i < 4; ++i) acc[i] = T2{0.f, 0.f};
+              for (int c = 0; c < QW; ++c) g[c] = gd[c];
 #pragma unroll
-              for (int r = 0; r < 7; ++r) {
-                const T2* gr = gcol + (size_t)(mir ? row0 - u1 - r : u1 + r + row0) * S;
-                T2 g[7];
+              for (int i = 0; i < 4; ++i) {
+                T2 sacc = T2{0.f, 0.f};
 #pragma unroll
-                for (int c = 0; c < 7; ++c) g[c] = gr[c];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  T2 sacc = T2{0.f, 0.f};
-#pragma unroll
-                  for (int c = 0; c < 7; ++c) sacc = rfma(yq[i][c], g[c], sacc);
-                  acc[i] = rfma(xq[i][r], sacc, acc[i]);
-                }
+                for (int c = 0; c < QW; ++c) sacc = rfma(y[i][c], g[c], sacc);
+                ad[i] = rfma(x[i], sacc, ad[i]);
               }
-              if (!mir) {
-                Pol[(int64_t)jq * half + lq] = acc[0];
-                Pol[(int64_t)jq * half + lq + 1] = acc[1];
-                Pol[(int64_t)(jq + 1) * half + lq] = acc[2];
-                Pol[(int64_t)(jq + 1) * half + lq + 1] = acc[3];
-              } else {
-                Pol[(int64_t)jq * half + (half - lq)] = acc[0];
-                Pol[(int64_t)jq * half + (half - lq - 1)] = acc[1];
-                Pol[(int64_t)(jq + 1) * half + (half - lq)] = acc[2];
-                Pol[(int64_t)(jq + 1) * half + (half - lq - 1)] = acc[3];
+#pragma unroll
+              for (int c = 0; c < QW; ++c) g[c] = gm[c];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                T2 sacc = T2{0.f, 0.f};
+#pragma unroll
+                for (int c = 0; c < QW; ++c) sacc = rfma(y[i][c], g[c], sacc);
+                am[i] = rfma(x[i], sacc, am[i]);
               }
             }
+            T2* pa = Pol + (int64_t)jq * half;
+            T2* pc = pa + half;
+            pa[lq] = ad[0]; pa[lq + sq] = ad[1]; pc[lq] = ad[2]; pc[lq + sq] = ad[3];
+            pa[half - lq] = am[0]; pa[half - lq - sq] = am[1]; pc[half - lq] = am[2]; pc[half - lq - sq] = am[3];
           }
         }
-#endif
         // double entries: nodes a, b of one ring (+ their mirrors) over one shared 7 x 7 window at U
         const int db = pp.phase_dbl_begin[ph], de = pp.phase_dbl_begin[ph + 1];
         // records are loaded one iteration ahead (an L2 round trip per entry was the loop's top stall)
@@ -527,16 +554,19 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             aa = rfma(xa[r], sa, aa); ab = rfma(xb[r], sb, ab);
             ma = rfma(xa[r], na, ma); mb = rfma(xb[r], nb2, mb);
           }
-          const int ja = int(uint32_t(r1.x) >> 16), la = r1.x & 0xFFFF, lb = r1.w & 0xFFFF;
-          // nodes a, b are (ja, la), (ja, lb); their mirrors (ja, half - la), (ja, half - lb).  Adjacent (lb = la + 1,
-          // rings sampled at every angle): half is even, so exactly one of the two adjacent pairs starts 16-byte
-          // aligned and is one 16-byte store.  Strided rings (lb = la + s_j): four 8-byte stores.
+          const int ja = int(uint32_t(r1.x) >> 16), la = r1.x & 0xFFFF;
+          const int jb = int(uint32_t(r1.w) >> 16), lb = r1.w & 0xFFFF;
+          // nodes a, b are (ja, la), (jb, lb); their mirrors (ja, half - la), (jb, half - lb).  Ring neighbours
+          // (jb = ja, lb = la + 1; rings sampled at every angle): half is even, so exactly one of the two adjacent
+          // pairs starts 16-byte aligned and is one 16-byte store.  Otherwise (strided rings, cross-ring pairs): four
+          // 8-byte stores.
           T2* prow = Pol + (int64_t)ja * half;
-          if (lb != la + 1) {
+          if (jb != ja || lb != la + 1) {
+            T2* prowb = Pol + (int64_t)jb * half;
             prow[la] = aa;
-            prow[lb] = ab;
+            prowb[lb] = ab;
             prow[half - la] = ma;
-            prow[half - lb] = mb;
+            prowb[half - lb] = mb;
           } else if (la & 1) {
             prow[la] = aa;
             prow[la + 1] = ab;
@@ -660,10 +690,13 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           float2 v[16];
 #pragma unroll
           for (int t1 = 0; t1 < 16; ++t1) {             // V (h = 1): times w^t; U: times 1 (selects, no branch)
-            const T2 tw = twT[16 * t1 + q];
+            // volatile shared load: loop-invariant, but hoisting 16 twiddles out of the group loop would pin 32
+            // registers for the whole angular pass (spills)
+            T2 tw;
+            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(tw.x), "=f"(tw.y)
+                         : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(twT + 16 * t1 + q))));
             v[t1] = cmul(float2{pfa[t1], pfb[t1]}, float2{h ? tw.x : 1.f, h ? tw.y : 0.f});
           }
-          load_pair(j0 + G);                          // next group's inputs, consumed one iteration later
           fft256_hw<false>(v, mybuf, twM, q);
           hw_store_natural(v, mybuf, q);
           __syncwarp();
@@ -677,6 +710,9 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             stg[sidx(2 * m + h, jj)] = h ? T2{-sp.y, sp.x} : sp;
             if (two) stg[sidx(2 * m + h, jj + 1)] = h ? dm : T2{dm.y, -dm.x};
           }
+          // next group's inputs, consumed one iteration later: issued after this group's FFT (the 32 prefetch
+          // registers are not live across it), in flight during the write-out
+          load_pair(j0 + G);
           __syncwarp();
           PROF_MARK(6);
         }

@@ -390,10 +390,6 @@ fbspca_status build_host_plan(Plan& P) {
       ph_quad(phase_lo.size());
   std::vector<uint32_t> singles;
   std::vector<std::array<uint32_t, 2>> dbl;
-  // Quad entries (same kernels): pair leaders (j, l), (j, l + 1), (j + 1, l), (j + 1, l + 1) of two adjacent rings
-  // whose four anchors differ by at most 1 in each direction share one (w + 1) x (w + 1) window: 49 grid loads for
-  // the four direct nodes and 49 for their four mirrors -- half the loads per node of a double entry.  Formed
-  // greedily over ring pairs (j even) before the doubles; their leaders are skipped below.
   // Angular stride per ring (M = 256 fp32 kernel).  Ring j only feeds K4 blocks k <= kneed(j) = max{k : kj0[k] <= j},
   // and F restricted to the ring has no angular content beyond kc(j): by Jacobi-Anger its k-th angular Fourier
   // coefficient is sum_x I(x) (-i)^k J_k(2 pi xi_j |x|) e^{-i k phi_x}, and |J_k(z)| < 1e-10 for k >= kc(z) past the
@@ -419,30 +415,42 @@ fbspca_status build_host_plan(Plan& P) {
       P.ring_s[j] = sj;
     }
   }
-  std::vector<std::array<uint32_t, 1>> quad;                 // (j << 16) | l of the first leader
+  // Quad entries (M = 256 fp32 kernel): pair leaders a = (j, l), b = (j, l + s), c = (j + 1, l), d = (j + 1, l + s) of
+  // two adjacent rings with the same stride s whose four anchors lie within kQuadW - w of each other in both directions
+  // share one kQuadW x kQuadW window at U = min anchors: 2 kQuadW^2 grid loads for the four direct nodes and their
+  // four mirrors (theta -> pi - theta): 12.25 loads per node at kQuadW = 7 against 24.5 for a double entry.  Each
+  // node's 6 x 6 taps sit at offsets (o1, o2) of the window; the kernel evaluates the window weights at all kQuadW
+  // positions and zeroes those outside the support.  Formed greedily along each even ring pair before the doubles
+  // (C3: 47 % of the pair leaders at kQuadW = 7, 97 % at 8).  FBSPCA_NO_QUADS=1 leaves everything to doubles / singles.
+  std::vector<std::array<uint32_t, 1>> quad;                 // (j << 16) | l of leader a
   std::vector<char> in_quad(size_t(P.n_xi) * (half + 1), 0);
-  // measured on B200 (C3): quads cut the gather's shared wavefronts 12 % but ran 2-4 % slower (more registers: spills in
-  // the ring pass, more bank conflicts among the fewer doubles) -- kept behind FBSPCA_QUADS=1 for experiments
-  // (the kernel's quad loop is compiled only with -DFBSPCA_QUAD_GATHER)
-  const bool quads = doubles && getenv("FBSPCA_QUADS") && atoi(getenv("FBSPCA_QUADS")) == 1 &&
-                     *std::max_element(P.ring_s.begin(), P.ring_s.end()) == 1;
+  auto phase_of_quad = [&](int u2) {       // all w + 2 columns must be valid grid columns of the phase
+    const int p = (u2 - b2min) / (S - w + 1);
+    if (p >= (int)phase_lo.size()) return -1;
+    const int last = std::min(phase_lo[p] + S - 1, b2max + w - 1);
+    return (u2 + kQuadW - 1 <= last) ? p : -1;
+  };
+  const bool quads = doubles && hw16 && kQuadW >= w && !getenv("FBSPCA_NO_QUADS");
   if (quads)
-    for (int j = 0; j + 1 < P.n_xi; j += 2)
-      for (int l = 1; 2 * (l + 1) < half;) {
-        const auto a = anchor(j, l), b = anchor(j, l + 1), c2 = anchor(j + 1, l), d = anchor(j + 1, l + 1);
+    for (int j = 0; j + 1 < P.n_xi; j += 2) {
+      const int sj = P.ring_s[j];
+      if (P.ring_s[j + 1] != sj) continue;
+      for (int l = sj; 2 * (l + sj) < half;) {
+        const auto a = anchor(j, l), b = anchor(j, l + sj), c2 = anchor(j + 1, l), d = anchor(j + 1, l + sj);
         const int lo1 = std::min({a.first, b.first, c2.first, d.first}), hi1 = std::max({a.first, b.first, c2.first, d.first});
         const int lo2 = std::min({a.second, b.second, c2.second, d.second}), hi2 = std::max({a.second, b.second, c2.second, d.second});
-        const int p = phase_of_double(lo2);
-        if (hi1 - lo1 <= 1 && hi2 - lo2 <= 1 && p >= 0) {
+        const int p = phase_of_quad(lo2);
+        if (hi1 - lo1 <= kQuadW - w && hi2 - lo2 <= kQuadW - w && p >= 0) {
           ph_quad[p].push_back({lo1, lo2, int(quad.size())});
           quad.push_back({(uint32_t(j) << 16) | uint32_t(l)});
           for (int dj = 0; dj < 2; ++dj)
-            for (int dl = 0; dl < 2; ++dl) in_quad[size_t(j + dj) * (half + 1) + l + dl] = 1;
-          l += 2;
+            for (int dl = 0; dl < 2; ++dl) in_quad[size_t(j + dj) * (half + 1) + l + dl * sj] = 1;
+          l += 2 * sj;
         } else {
-          ++l;
+          l += sj;
         }
       }
+    }
   for (int j = 0; j < P.n_xi; ++j) {
     const int sj = P.ring_s[j];               // ring j's angles theta_l, l = 0, sj, 2 sj, .. (sj | half/2)
     for (int l = 0; 2 * l <= half; l += sj) {
@@ -459,9 +467,54 @@ fbspca_status build_host_plan(Plan& P) {
           continue;
         }
       }
-      ph_single[phase_of_single(a.second)].push_back({a.first, a.second, int(singles.size())});
       singles.push_back((uint32_t(j) << 16) | uint32_t(l));
     }
+  }
+  // Leftover pair leaders (no ring neighbour within reach) are paired across rings: any two whose anchors differ by
+  // at most 1 in each direction share a 7 x 7 window just as ring neighbours do (the double-entry kernel takes each
+  // node's ring from its record).  A single costs 36 grid loads per node, a double 24.5.
+  if (doubles) {
+    std::vector<char> paired(singles.size(), 0);
+    std::vector<std::pair<std::pair<int, int>, int>> by_anchor;       // (anchor, index) of mirrored leaders
+    for (size_t i = 0; i < singles.size(); ++i) {
+      const int j = int(singles[i] >> 16), l = int(singles[i] & 0xffffu);
+      if (l >= 1 && 2 * l < half) by_anchor.push_back({anchor(j, l), int(i)});
+    }
+    std::sort(by_anchor.begin(), by_anchor.end());
+    auto find = [&](std::pair<int, int> an) {
+      auto it = std::lower_bound(by_anchor.begin(), by_anchor.end(), std::make_pair(an, -1));
+      for (; it != by_anchor.end() && it->first == an; ++it)
+        if (!paired[it->second]) return it->second;
+      return -1;
+    };
+    for (auto& e : by_anchor) {
+      const int i = e.second;
+      if (paired[i]) continue;
+      paired[i] = 1;
+      int mate = -1;
+      for (int d1 = -1; d1 <= 1 && mate < 0; ++d1)
+        for (int d2 = -1; d2 <= 1 && mate < 0; ++d2) {
+          const int m = find({e.first.first + d1, e.first.second + d2});
+          if (m < 0) continue;
+          const int u2 = std::min(e.first.second, e.first.second + d2);
+          if (phase_of_double(u2) >= 0) mate = m;
+        }
+      if (mate < 0) { paired[i] = 0; continue; }
+      paired[mate] = 1;
+      const int j = int(singles[mate] >> 16), l = int(singles[mate] & 0xffffu);
+      const auto b = anchor(j, l);
+      const int u1 = std::min(e.first.first, b.first), u2 = std::min(e.first.second, b.second);
+      ph_double[phase_of_double(u2)].push_back({u1, u2, int(dbl.size())});
+      dbl.push_back({singles[i], singles[mate]});
+    }
+    std::vector<uint32_t> rest;
+    for (size_t i = 0; i < singles.size(); ++i)
+      if (!paired[i]) rest.push_back(singles[i]);
+    singles.swap(rest);
+  }
+  for (size_t i = 0; i < singles.size(); ++i) {
+    const auto a = anchor(int(singles[i] >> 16), int(singles[i] & 0xffffu));
+    ph_single[phase_of_single(a.second)].push_back({a.first, a.second, int(i)});
   }
   P.nodes.clear();
   P.dnoderec.clear();
@@ -473,11 +526,11 @@ fbspca_status build_host_plan(Plan& P) {
     pp.phase_dbl_begin[np] = int(P.dnoderec.size() / 8);
     pp.phase_quad_begin[np] = int(P.qnoderec.size() / 12);
     for (uint32_t id : pack_gather_items(ph_quad[p], S)) {
-      // {U1 | U2 << 16, offsets (2 bits per node: o1 | o2 << 1), (j << 16) | l, 0}, {t1, t2} of nodes a, b, c, d
-      // (a = (j, l), b = (j, l + 1), c = (j + 1, l), d = (j + 1, l + 1)); t = k - b of each node's own anchor
+      // {U1 | U2 << 16, offsets (o1 | o2 << 2 in 4 bits per node) | s << 16, (j << 16) | l, 0}, {t1' of a, b, c, d},
+      // {t2' of a, b, c, d}: t' = k - U = (k - b) + o, the node's distance from the window's first row / column
       const uint32_t nd = quad[id][0];
-      const int j = int(nd >> 16), l = int(nd & 0xffffu);
-      const int jj[4] = {j, j, j + 1, j + 1}, ll[4] = {l, l + 1, l, l + 1};
+      const int j = int(nd >> 16), l = int(nd & 0xffffu), sj = P.ring_s[j];
+      const int jj[4] = {j, j, j + 1, j + 1}, ll[4] = {l, l + sj, l, l + sj};
       std::pair<int, int> an[4];
       int u1 = 1 << 30, u2 = 1 << 30;
       for (int i = 0; i < 4; ++i) { an[i] = anchor(jj[i], ll[i]); u1 = std::min(u1, an[i].first); u2 = std::min(u2, an[i].second); }
@@ -485,12 +538,13 @@ fbspca_status build_host_plan(Plan& P) {
       rec[0] = int32_t((uint32_t(u1) & 0xFFFFu) | (uint32_t(u2) << 16));
       int of = 0;
       for (int i = 0; i < 4; ++i) {
-        of |= ((an[i].first - u1) | ((an[i].second - u2) << 1)) << (2 * i);
-        const float t1 = float(rho[jj[i]] * cs[2 * ll[i]] - an[i].first), t2 = float(rho[jj[i]] * cs[2 * ll[i] + 1] - an[i].second);
-        std::memcpy(&rec[4 + 2 * i], &t1, 4);
-        std::memcpy(&rec[5 + 2 * i], &t2, 4);
+        const int o1 = an[i].first - u1, o2 = an[i].second - u2;
+        of |= (o1 | (o2 << 2)) << (4 * i);
+        const float t1 = float(rho[jj[i]] * cs[2 * ll[i]] - u1), t2 = float(rho[jj[i]] * cs[2 * ll[i] + 1] - u2);
+        std::memcpy(&rec[4 + i], &t1, 4);
+        std::memcpy(&rec[8 + i], &t2, 4);
       }
-      rec[1] = of;
+      rec[1] = of | (sj << 16);
       rec[2] = int32_t(nd);
       P.qnoderec.insert(P.qnoderec.end(), rec, rec + 12);
     }
