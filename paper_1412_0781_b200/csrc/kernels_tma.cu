@@ -106,12 +106,23 @@ __device__ __forceinline__ float4 lo_part(float4 x) {
 __device__ __forceinline__ void make_lo(const unsigned char* src, unsigned char* dst, int bytes, int tid) {
   const uint32_t s = su32(src), d = su32(dst);
   const int n = bytes >> 4;
-#pragma unroll 4
-  for (int i = tid; i < n; i += 128) {
-    float4 x;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(s + 16 * i));
-    x = lo_part(x);
-    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(d + 16 * i), "f"(x.x), "f"(x.y), "f"(x.z), "f"(x.w) : "memory");
+  // four granules in flight per thread (one load / store pair at a time left every load's latency exposed)
+  for (int i0 = tid; i0 < n; i0 += 4 * 128) {
+    float4 x[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = min(i0 + j * 128, n - 1);
+      asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x[j].x), "=f"(x[j].y), "=f"(x[j].z), "=f"(x[j].w)
+          : "r"(s + 16 * i) : "memory");
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (i0 + j * 128 < n) {
+        const float4 y = lo_part(x[j]);
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(d + 16 * (i0 + j * 128)), "f"(y.x), "f"(y.y),
+                     "f"(y.z), "f"(y.w) : "memory");
+      }
+    }
   }
 }
 
@@ -482,13 +493,40 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
       const int kc0 = si * CK * e.G, nkc_here = min(nt * e.G, e.nkc - kc0);
       unsigned char* st = sm + s * stage_bytes;
       bar_wait(&full[s], (it / NS) & 1);
-      for (int u = 0; u < nt * e.G; ++u) {
-        unsigned char* xu = st + (u / e.G) * tile_bytes + (u % e.G) * 2 * b * ROWB;
-        if (u >= nkc_here) {                                 // ragged end of the item: no chunk loaded, zero it
+      if (nkc_here < nt * e.G) {                             // ragged end of the item: chunks not loaded, zero them
+        for (int u = nkc_here; u < nt * e.G; ++u) {
+          unsigned char* xu = st + (u / e.G) * tile_bytes + (u % e.G) * 2 * b * ROWB;
           for (int i = tid; i < b * KC; i += 128) reinterpret_cast<float*>(xu)[i] = 0.f;
-          named_sync(1, 128);
         }
-        make_lo(xu, xu + b * ROWB, b * ROWB, tid);
+        named_sync(1, 128);
+      }
+      {
+        // lo parts of all chunks of the stage as one flat loop, four 16-byte granules in flight per thread
+        // (the chunk-by-chunk loop with volatile loads waited on every granule: shared latency bound)
+        const int lg_per = 3 + box_idx(b) + 4;                 // log2(8 b): granules per chunk (b rows x 128 B)
+        const int lg_g = 31 - __clz(e.G);
+        const int ntot = (nt * e.G) << lg_per;
+        const uint32_t sbase = su32(st);
+        for (int f0 = tid; f0 < ntot; f0 += 4 * 128) {
+          float4 x[4];
+          uint32_t ad[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int f = min(f0 + j * 128, ntot - 1);
+            const int u = f >> lg_per, i = f & ((1 << lg_per) - 1);
+            ad[j] = sbase + uint32_t((u >> lg_g) * tile_bytes + (u & (e.G - 1)) * 2 * b * ROWB + 16 * i);
+            asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x[j].x), "=f"(x[j].y), "=f"(x[j].z), "=f"(x[j].w)
+                : "r"(ad[j]) : "memory");
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (f0 + j * 128 < ntot) {
+              const float4 y = lo_part(x[j]);
+              asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(ad[j] + uint32_t(b * ROWB)), "f"(y.x),
+                           "f"(y.y), "f"(y.z), "f"(y.w) : "memory");
+            }
+          }
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       bar_arrive(&loready[s]);
