@@ -93,6 +93,17 @@ fbspca_status fbspca_plan_detail(fbspca_plan_t plan, int* M, int* w, double* bet
                                  int* smem_bytes, const double** zeros, const double** xi,
                                  const double** wq);
 
+/* Host-side plan query (no device work): the angular sampling of each ring and K4's first ring per k.
+ *   ring_stride  n_xi ints (caller-owned, may be NULL): s_j -- ring j is sampled at theta_l = 2 pi l / n_theta for
+ *                l = 0, s_j, 2 s_j, .. (n_theta / s_j angles).  s_j > 1 only for the M = 256 fp32 kernel, where
+ *                n_theta / s_j >= kneed(j) + kc(j) keeps every coefficient the ring feeds free of angular aliases
+ *                (kc: the Bessel band limit of the image's angular content on the ring, reading Q21 of DESIGN.md);
+ *                the paper's grid (Eq. (1DFFT)) is s_j = 1.
+ *   k_first_ring k_max + 1 ints (caller-owned, may be NULL): kj0[k], the first ring of Eq. (a)'s sum K4 reads for
+ *                block k (rings below carry |T_k| < 1e-9 max |T_k|; 0 for fp64 plans).
+ * Errors: FBSPCA_ERR_ARG for a null plan. */
+fbspca_status fbspca_plan_rings(fbspca_plan_t plan, int* ring_stride, int* k_first_ring);
+
 /* Alg. 1 lines 3-4: a = T* I for n images.  NUFFT (K1 pad+deapodise+2-D FFT, K2 window gather
  * to the half-plane polar nodes), K3 angular FFT (Eq. (1DFFT)), K4 radial quadrature (Eq. (a)).
  *   d_images  n x L x L (float or double per dt), device.   d_coeffs  sum_k p_k x n complex (coefficient

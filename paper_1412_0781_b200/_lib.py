@@ -24,6 +24,7 @@ SIGNATURES = {
                                  ctypes.POINTER(P_int64), ctypes.POINTER(P_int64)]),
     "fbspca_plan_detail": (c_int, [c_void_p, P_int, P_int, P_double, P_int, P_int, ctypes.POINTER(P_double),
                                    ctypes.POINTER(P_double), ctypes.POINTER(P_double)]),
+    "fbspca_plan_rings": (c_int, [c_void_p, c_void_p, c_void_p]),
     "fbspca_expand": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "fbspca_covariance": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "fbspca_covariance_partial": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),

@@ -386,6 +386,13 @@ fbspca_status fbspca_plan_detail(fbspca_plan_t h, int* M, int* w, double* beta, 
   return FBSPCA_OK;
 }
 
+fbspca_status fbspca_plan_rings(fbspca_plan_t h, int* ring_stride, int* k_first_ring) {
+  if (!h) { set_error("null plan"); return FBSPCA_ERR_ARG; }
+  if (ring_stride) std::copy(h->ring_s.begin(), h->ring_s.end(), ring_stride);
+  if (k_first_ring) std::copy(h->kj0.begin(), h->kj0.end(), k_first_ring);
+  return FBSPCA_OK;
+}
+
 fbspca_status fbspca_expand(fbspca_plan_t h, const void* d_images, int64_t n, void* d_coeffs, fbspca_stream_t stream) {
   fbspca_status st = check_compute_plan(h);
   if (st != FBSPCA_OK) return st;

@@ -112,6 +112,14 @@ def fbspca_plan(L: int, c: float, R: float, eps: float = 0.0, dtype: int = F32, 
                 wq=np.ctypeslib.as_array(wp, shape=(n_xi.value,)).copy())
 
 
+def fbspca_plan_rings(plan: Plan):
+    """(ring_stride[n_xi], k_first_ring[k_max + 1]) of the plan (include/fbspca.h: fbspca_plan_rings)."""
+    rs = np.zeros(plan.n_xi, dtype=np.int32)
+    kj = np.zeros(plan.k_max + 1, dtype=np.int32)
+    check(lib().fbspca_plan_rings(ctypes.c_void_p(plan.handle), rs.ctypes.data, kj.ctypes.data), "fbspca_plan_rings")
+    return rs, kj
+
+
 def _on_plan_device(plan: Plan, *tensors):
     for t in tensors:
         if t.device.type != "cuda" or t.device.index != plan.device:

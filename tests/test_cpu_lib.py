@@ -118,3 +118,58 @@ def test_unpack_blocks_layout():
         packed[pl.blk_off[k]:pl.blk_off[k + 1]] = A[np.triu_indices(pk)]
     got = F.unpack_blocks(pl, packed)
     assert all(np.array_equal(a, b) for a, b in zip(got, mats))
+
+
+def _strided_angular(Fp, rs, k_max):
+    """Eq. (1DFFT) on ring j sampled at every rs[j]-th angle: (2 pi s / n_theta) sum_{l = 0, s, 2s..} F e^{-ik theta_l},
+    i.e. the (n_theta / s)-point DFT of the subsampled ring, indexed k mod (n_theta / s)."""
+    n, n_xi, nt = Fp.shape
+    out = np.empty((n, n_xi, k_max + 1), dtype=np.complex128)
+    k = np.arange(k_max + 1)
+    for j in range(n_xi):
+        s = int(rs[j])
+        nj = nt // s
+        out[:, j, :] = (2 * np.pi / nj) * np.fft.fft(Fp[:, j, ::s], axis=-1)[:, k % nj]
+    return out
+
+
+def test_ring_stride_reading_against_oracle():
+    """Reading Q21: the M = 256 plan samples inner rings at n_theta / s_j angles.  Against the oracle's
+    exact direct sum (O5) on white-noise images (the most corner / high-angular content a square image has), ring j's
+    Eq. (1DFFT) values for every k it feeds (k <= kneed(j), i.e. kj0[k] <= j) agree with the paper's n_theta-angle
+    values to 1e-9 of the ring's largest value, and the Eq. (a) coefficients (K4's sum from kj0[k]) to 1e-8 rel l2 --
+    four orders below the fp32 NUFFT error the path is held to.  Doubling any stride breaks the bound (the check has
+    teeth: aliases of the ring's angular content land on the k it feeds)."""
+    pl = F.fbspca_plan(128, 0.5, 64, device=-1)
+    rs, kj0 = F.fbspca_plan_rings(pl)
+    assert rs.max() >= 4 and rs.min() == 1 and np.all(np.diff(rs) <= 0)
+    b = O.build_basis(0.5, 64)
+    assert b.n_theta == pl.n_theta and b.k_max == pl.k_max
+    imgs = np.random.default_rng(21).standard_normal((2, 128, 128))
+    Fp = O.polar_ft_direct(imgs, b)
+    g_full = O.angular_transform(Fp, b.k_max)
+    g_str = _strided_angular(Fp, rs, b.k_max)
+    kneed = np.array([max(k for k in range(b.k_max + 1) if kj0[k] <= j) for j in range(b.n_xi)])
+    worst = 0.0
+    for j in range(b.n_xi):
+        scale = np.abs(g_full[:, j, :]).max()
+        err = np.abs(g_str[:, j, :kneed[j] + 1] - g_full[:, j, :kneed[j] + 1]).max() / scale
+        worst = max(worst, err)
+    assert worst < 1e-9, worst
+    # Eq. (a): K4 sums block k from ring kj0[k] on the strided rings
+    table = O.radial_table(b)
+    A_full = O.radial_quadrature(g_full, b, table)
+    tab_cut = [t.copy() for t in table]
+    for k in range(b.k_max + 1):
+        tab_cut[k][:, :kj0[k]] = 0.0
+    A_str = O.radial_quadrature(g_str, b, tab_cut)
+    full, got = O.to_flat(A_full), O.to_flat(A_str)
+    rel = np.linalg.norm(got - full, axis=0) / np.linalg.norm(full, axis=0)
+    assert rel.max() < 1e-8, rel.max()
+    # teeth: twice the plan's stride on the outermost ring of a stride class aliases visibly
+    rs2 = rs.copy()
+    j2 = int(np.nonzero(rs == 2)[0][-1])           # last ring the plan samples at every second angle
+    rs2[j2] = 4
+    g_bad = _strided_angular(Fp[:, j2:j2 + 1, :], rs2[j2:j2 + 1], b.k_max)
+    bad = np.abs(g_bad[:, 0, :kneed[j2] + 1] - g_full[:, j2, :kneed[j2] + 1]).max() / np.abs(g_full[:, j2, :]).max()
+    assert bad > 1e-6, bad
