@@ -727,7 +727,11 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           const bool two = jj + 1 < g;
           const T2* fa = Pol + (int64_t)(j0 + jj) * half;
           const T2* fb = two ? fa + half : fa;
-          auto ldu = [&](int t) -> T2 { const T2 a = fa[t], b = fb[t]; return T2{a.x, two ? b.x : T(0)}; };
+          // rings sampled at every s_j-th angle (reading Q21): the other positions are zeros of the stuffed ring
+          const int ma = __ldg(pp.ring_s + j0 + jj) - 1, mb = two ? __ldg(pp.ring_s + j0 + jj + 1) - 1 : 0;
+          auto ring_a = [&](int t) -> T2 { return (t & ma) ? T2{T(0), T(0)} : fa[t]; };
+          auto ring_b = [&](int t) -> T2 { return (two && !(t & mb)) ? fb[t] : T2{T(0), T(0)}; };
+          auto ldu = [&](int t) -> T2 { return T2{ring_a(t).x, ring_b(t).x}; };
           fft_ct<T2, MC, false, FG>(ldu, stR, myA, myB, twM, glane, gbar);
           gsync<FG>(gbar);
           for (int m = glane; 2 * m <= kmx; m += FG) {
@@ -739,10 +743,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             if (two) stg[sidx(2 * m, jj + 1)] = T2{dm.y, -dm.x};
           }
           gsync<FG>(gbar);
-          auto ldv = [&](int t) -> T2 {
-            const T2 a = fa[t], b = fb[t];
-            return cmul(T2{a.y, two ? b.y : T(0)}, twT[t]);
-          };
+          auto ldv = [&](int t) -> T2 { return cmul(T2{ring_a(t).y, ring_b(t).y}, twT[t]); };
           fft_ct<T2, MC, false, FG>(ldv, stR, myA, myB, twM, glane, gbar);
           gsync<FG>(gbar);
           for (int m = glane; 2 * m + 1 <= kmx; m += FG) {

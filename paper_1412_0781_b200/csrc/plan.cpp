@@ -390,7 +390,7 @@ fbspca_status build_host_plan(Plan& P) {
       ph_quad(phase_lo.size());
   std::vector<uint32_t> singles;
   std::vector<std::array<uint32_t, 2>> dbl;
-  // Angular stride per ring (M = 256 fp32 kernel).  Ring j only feeds K4 blocks k <= kneed(j) = max{k : kj0[k] <= j},
+  // Angular stride per ring (fp32 compile-time ring-pair kernels: M in {64, 128, 256, 512, 600, 720}).  Ring j only feeds K4 blocks k <= kneed(j) = max{k : kj0[k] <= j},
   // and F restricted to the ring has no angular content beyond kc(j): by Jacobi-Anger its k-th angular Fourier
   // coefficient is sum_x I(x) (-i)^k J_k(2 pi xi_j |x|) e^{-i k phi_x}, and |J_k(z)| < 1e-10 for k >= kc(z) past the
   // turning point, with |x| <= r_c = sqrt(2) ceil(L/2) over the square (no disk mask, reading Q7).  Sampling the ring
@@ -400,7 +400,8 @@ fbspca_status build_host_plan(Plan& P) {
   // 2 pi s_j / n_theta is the table's 2 pi / n_theta times the power of two s_j (capi.cu upload).  Inner rings need
   // far fewer angles: C3 gathers 0.70 of the nodes.  FBSPCA_NO_RING_STRIDE=1 samples every ring at all n_theta angles.
   P.ring_s.assign(P.n_xi, 1);
-  if (hw16 && !getenv("FBSPCA_NO_RING_STRIDE")) {
+  const bool ring_stride_kernel = P.dt == FBSPCA_F32 && w == 6 && pow2_kernel && P.n_theta == 2 * M;
+  if (ring_stride_kernel && !getenv("FBSPCA_NO_RING_STRIDE")) {
     const double rc = std::sqrt(2.0) * std::ceil(0.5 * L);
     for (int j = 0; j < P.n_xi; ++j) {
       int kneed = 0;
