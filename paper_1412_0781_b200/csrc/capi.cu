@@ -268,7 +268,6 @@ fbspca_status upload_plan(Plan& P) {
   FB_CUDA(upload((void**)&P.d_ring_s, P.ring_s.data(), P.ring_s.size()), "upload ring strides");
   FB_CUDA(upload((void**)&P.d_noderec, P.noderec.data(), P.noderec.size()), "upload node records");
   FB_CUDA(upload((void**)&P.d_dnoderec, P.dnoderec.data(), P.dnoderec.size()), "upload double node records");
-  FB_CUDA(upload((void**)&P.d_qnoderec, P.qnoderec.data(), P.qnoderec.size()), "upload quad node records");
   PolarParams& pp = P.pp;
   pp.xscratch_stride = (int64_t)P.L * pp.ncols_x;
   pp.pscratch_stride = (int64_t)P.n_xi * pp.half;
@@ -295,7 +294,6 @@ fbspca_status upload_plan(Plan& P) {
   pp.rho = P.d_rho; pp.cs = P.d_cs; pp.nodes = P.d_nodes; pp.kj0 = P.d_kj0; pp.ring_s = P.d_ring_s;
   pp.noderec = reinterpret_cast<const int4*>(P.d_noderec);
   pp.dnoderec = reinterpret_cast<const int4*>(P.d_dnoderec);
-  pp.qnoderec = reinterpret_cast<const int4*>(P.d_qnoderec);
   pp.xscratch = P.d_xscratch; pp.pscratch = P.d_pscratch;
   FB_CUDA(upload((void**)&P.d_pp, &pp, 1), "upload polar params");
   return FBSPCA_OK;
@@ -308,7 +306,7 @@ void free_plan(Plan& P) {
                   P.d_pscratch, P.d_ghat, P.d_partial, P.d_p, P.d_coef_off, P.d_blk_off, P.d_evec_off,
                   P.d_eig_work, P.d_eig_sweeps, P.d_coef_k, P.d_pp, P.d_cov_scratch, P.d_cov_scratch0, P.d_table_hi, P.d_table_lo, P.d_rbasis,
                   P.d_synth_rho, P.d_synth_pidx, P.d_synth_pir, P.d_synth_pcs, P.d_synth_grp,
-                  P.d_noderec, P.d_dnoderec, P.d_kj0, P.d_qnoderec, P.d_ring_s};
+                  P.d_noderec, P.d_dnoderec, P.d_kj0, P.d_ring_s};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (cudaEvent_t e : P.event_pool) cudaEventDestroy(e);
   P.event_pool.clear();

@@ -26,13 +26,6 @@ constexpr int kCovMaxSub0 = kCovBatchTc / kCovChunk0;
 // Per-warp FFT scratch of the polar kernel (complex elements): two ping-pong buffers of M (padded to 16), or for the
 // M = 256 fp32 kernel (hw: half-warp radix-16 x 16 FFTs, fft_device.cuh) two half-warp buffers of 16 rows x 17.
 constexpr int kHwBuf = 272;
-// Quad gather entries (M = 256 fp32 kernel, plan.cpp): four pair leaders share one kQuadW x kQuadW window
-// (anchors within kQuadW - 6 of each other; 7: no padded taps, 8: more leaders grouped, 1/3 more taps and weights).
-// Measured on B200 (C3 polar, same box A/B): none 45.98 ms, 7 x 7 49.2 ms, 8 x 8 52.2 ms -- off (0) by default.
-#ifndef FBSPCA_QUAD_W
-#define FBSPCA_QUAD_W 0
-#endif
-constexpr int kQuadW = FBSPCA_QUAD_W;
 __host__ __device__ constexpr int polar_warp_scratch(int M, bool hw) { return hw ? 2 * kHwBuf : 2 * ((M + 15) & ~15); }
 
 // Stockham radix plan for a length-N FFT (N = prod radices; radices in {2,3,4,5,8}).
@@ -51,7 +44,6 @@ struct PolarParams {
   int phase_lo[kMaxPhases];       // first column (m2) of phase p
   int phase_node_begin[kMaxPhases + 1];
   int phase_dbl_begin[kMaxPhases + 1];       // double entries (2 int4 each) of phase p: [begin[p], begin[p+1])
-  int phase_quad_begin[kMaxPhases + 1];      // quad entries (3 int4 each) of phase p
   double beta;
   double half_w;                  // w/2
   int nwarps;                     // warps per CTA (gather, fills)
@@ -76,7 +68,6 @@ struct PolarParams {
   const int* ring_s;              // per ring j: angular stride s_j (ring sampled at theta_l, l = 0, s_j, 2 s_j, ..; plan.cpp)
   const int4* noderec;            // per entry {b1 | b2 << 16, t1, t2, (j << 16) | l} (fp32 path)
   const int4* dnoderec;           // per double entry 2 int4 (plan.cpp "Double entries")
-  const int4* qnoderec;           // per quad entry 3 int4 (plan.cpp "Quad entries")
   void* xscratch;                 // per resident CTA: L x ncols_x complex
   void* pscratch;                 // per resident CTA: n_xi x half complex
   int64_t ghat_kstride;           // ghat elements (T) per k: 2 max_batch n_xi (fixed, so one TMA map serves all batches)
@@ -116,8 +107,6 @@ struct Plan {
   std::vector<uint32_t> nodes;
   std::vector<int32_t> noderec;          // 4 per node entry
   std::vector<int32_t> dnoderec;         // 8 per double entry
-  std::vector<int32_t> qnoderec;         // 12 per quad entry
-  int32_t* d_qnoderec = nullptr;
   int polar_smem = 0;
   int polar_grid = 0;                    // resident CTAs of the polar kernel
   // device buffers

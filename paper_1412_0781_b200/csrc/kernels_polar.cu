@@ -66,28 +66,6 @@ template <> struct Es<float> {
     const float s = sqrt_approx(fmaxf(fmaf(-z, z, 1.f), 0.f));
     return ex2_approx(fmaf(s, bl, -bl));
   }
-  // phi(ta - q), phi(tb - q), exactly 0 outside the support |d| < hw (quad windows: 8 positions, 6 taps per node)
-  __device__ __forceinline__ void pair_masked(float ta, float tb, float q, float& pa, float& pb) const {
-    const float hw = 1.f / inv_hw, hw2 = hw * hw, blh = bl * inv_hw;
-    unsigned long long t, qq, d, dn, r, e, c2, h2, b2;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(t) : "f"(ta), "f"(tb));
-    asm("mov.b64 %0, {%1, %1};" : "=l"(qq) : "f"(q));
-    asm("mov.b64 %0, {%1, %1};" : "=l"(h2) : "f"(hw2));
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(t), "l"(qq));
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dn) : "l"(qq), "l"(t));
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(dn), "l"(d), "l"(h2));
-    float ra, rb;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(ra), "=f"(rb) : "l"(r));
-    const bool ina = ra > 0.f, inb = rb > 0.f;
-    const float sa = sqrt_approx(fabsf(ra)), sb = sqrt_approx(fabsf(rb));
-    asm("mov.b64 %0, {%1, %2};" : "=l"(e) : "f"(sa), "f"(sb));
-    asm("mov.b64 %0, {%1, %1};" : "=l"(c2) : "f"(blh));
-    asm("mov.b64 %0, {%1, %1};" : "=l"(b2) : "f"(-bl));
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(e), "l"(c2), "l"(b2));
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(ra), "=f"(rb) : "l"(r));
-    pa = ina ? ex2_approx(ra) : 0.f;
-    pb = inb ? ex2_approx(rb) : 0.f;
-  }
   // phi(ta - q), phi(tb - q) with packed f32x2 arithmetic: d = t - q, r = hw^2 - d^2 = (q - t) d + hw^2 (FADD2, FADD2,
   // FFMA2), e = ex2(bl s / hw - bl), s = sqrt|r| (the |.| only absorbs rounding at |d| = hw; FFMA2), 4 MUFU
   __device__ __forceinline__ void pair(float ta, float tb, float q, float& pa, float& pb) const {
@@ -441,71 +419,6 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       __syncthreads();
       PROF_MARK(2);
       if constexpr (sizeof(T) == 4 && W == 6 && MC > 0) {
-        if constexpr (HW && kQuadW > 0) {
-          // quad entries (plan.cpp): leaders a = (j, l), b = (j, l + s), c = (j + 1, l), d = (j + 1, l + s) over one
-          // shared QW x QW window at U (QW = kQuadW); per window row, the direct row U1 + r and the mirrored row
-          // -U1 - r are loaded once (2 QW grid loads) for all eight nodes.  Column weights y (4 nodes x QW positions)
-          // are held, row weights are evaluated per row; positions outside a node's 6 x 6 support get exactly 0.
-          constexpr int QW = kQuadW;
-          const int qb = pp.phase_quad_begin[ph], qe = pp.phase_quad_begin[ph + 1];
-          int4 q0 = make_int4(0, 0, 0, 0), q1 = q0, q2 = q0;     // records one iteration ahead
-          if (qb + tid < qe) {
-            q0 = __ldg(pp.qnoderec + 3 * (qb + tid)); q1 = __ldg(pp.qnoderec + 3 * (qb + tid) + 1);
-            q2 = __ldg(pp.qnoderec + 3 * (qb + tid) + 2);
-          }
-          for (int t = qb + tid; t < qe; t += nthr) {
-            const int4 r0 = q0, r1 = q1, r2 = q2;
-            if (t + nthr < qe) {
-              q0 = __ldg(pp.qnoderec + 3 * (t + nthr)); q1 = __ldg(pp.qnoderec + 3 * (t + nthr) + 1);
-              q2 = __ldg(pp.qnoderec + 3 * (t + nthr) + 2);
-            }
-            const int u1 = int(short(r0.x & 0xFFFF)), u2 = r0.x >> 16, sq = r0.y >> 16;
-            const int jq = int(uint32_t(r0.z) >> 16), lq = r0.z & 0xFFFF;
-            const float t1[4] = {__int_as_float(r1.x), __int_as_float(r1.y), __int_as_float(r1.z), __int_as_float(r1.w)};
-            const float t2[4] = {__int_as_float(r2.x), __int_as_float(r2.y), __int_as_float(r2.z), __int_as_float(r2.w)};
-            float y[4][QW];
-#pragma unroll
-            for (int c = 0; c < QW; ++c) {
-              phi.pair_masked(t2[0], t2[1], float(c), y[0][c], y[1][c]);
-              phi.pair_masked(t2[2], t2[3], float(c), y[2][c], y[3][c]);
-            }
-            const T2* gcol = Gc + (u2 - lo);
-            T2 ad[4], am[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) { ad[i] = T2{0.f, 0.f}; am[i] = ad[i]; }
-#pragma unroll 1
-            for (int r = 0; r < QW; ++r) {
-              float x[4];
-              phi.pair_masked(t1[0], t1[1], float(r), x[0], x[1]);
-              phi.pair_masked(t1[2], t1[3], float(r), x[2], x[3]);
-              const T2* gd = gcol + (size_t)(u1 + r + row0) * S;
-              const T2* gm = gcol + (size_t)(row0 - u1 - r) * S;
-              T2 g[QW];
-#pragma unroll
-              for (int c = 0; c < QW; ++c) g[c] = gd[c];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                T2 sacc = T2{0.f, 0.f};
-#pragma unroll
-                for (int c = 0; c < QW; ++c) sacc = rfma(y[i][c], g[c], sacc);
-                ad[i] = rfma(x[i], sacc, ad[i]);
-              }
-#pragma unroll
-              for (int c = 0; c < QW; ++c) g[c] = gm[c];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                T2 sacc = T2{0.f, 0.f};
-#pragma unroll
-                for (int c = 0; c < QW; ++c) sacc = rfma(y[i][c], g[c], sacc);
-                am[i] = rfma(x[i], sacc, am[i]);
-              }
-            }
-            T2* pa = Pol + (int64_t)jq * half;
-            T2* pc = pa + half;
-            pa[lq] = ad[0]; pa[lq + sq] = ad[1]; pc[lq] = ad[2]; pc[lq + sq] = ad[3];
-            pa[half - lq] = am[0]; pa[half - lq - sq] = am[1]; pc[half - lq] = am[2]; pc[half - lq - sq] = am[3];
-          }
-        }
         // double entries: nodes a, b of one ring (+ their mirrors) over one shared 7 x 7 window at U
         const int db = pp.phase_dbl_begin[ph], de = pp.phase_dbl_begin[ph + 1];
         // records are loaded one iteration ahead (an L2 round trip per entry was the loop's top stall)
@@ -554,27 +467,27 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             aa = rfma(xa[r], sa, aa); ab = rfma(xb[r], sb, ab);
             ma = rfma(xa[r], na, ma); mb = rfma(xb[r], nb2, mb);
           }
-          const int ja = int(uint32_t(r1.x) >> 16), la = r1.x & 0xFFFF;
-          const int jb = int(uint32_t(r1.w) >> 16), lb = r1.w & 0xFFFF;
-          // nodes a, b are (ja, la), (jb, lb); their mirrors (ja, half - la), (jb, half - lb).  Ring neighbours
-          // (jb = ja, lb = la + 1; rings sampled at every angle): half is even, so exactly one of the two adjacent
-          // pairs starts 16-byte aligned and is one 16-byte store.  Otherwise (strided rings, cross-ring pairs): four
-          // 8-byte stores.
+          // Pol slots (plan.cpp pol_slot): ring j holds its samples contiguously, mirror of slot l at half_j - l
+          const int ja = (r1.x >> 16) & 0xFFF, la = r1.x & 0xFFFF, ha = half >> ((uint32_t(r1.x) >> 28) & 3);
+          const int jb = (r1.w >> 16) & 0xFFF, lb = r1.w & 0xFFFF, hb = half >> ((uint32_t(r1.w) >> 28) & 3);
+          // nodes a, b are (ja, la), (jb, lb); their mirrors (ja, half_a - la), (jb, half_b - lb).  Ring neighbours
+          // (jb = ja, lb = la + 1) with an even half_j: exactly one of the two adjacent slot pairs starts 16-byte
+          // aligned and is one 16-byte store.  Otherwise (cross-ring pairs, odd half_j): four 8-byte stores.
           T2* prow = Pol + (int64_t)ja * half;
-          if (jb != ja || lb != la + 1) {
+          if (jb != ja || lb != la + 1 || (ha & 1)) {     // (odd half_j, e.g. 600 / 8: no aligned pair guaranteed)
             T2* prowb = Pol + (int64_t)jb * half;
             prow[la] = aa;
             prowb[lb] = ab;
-            prow[half - la] = ma;
-            prowb[half - lb] = mb;
+            prow[ha - la] = ma;
+            prowb[hb - lb] = mb;
           } else if (la & 1) {
             prow[la] = aa;
             prow[la + 1] = ab;
-            *reinterpret_cast<float4*>(prow + (half - la - 1)) = make_float4(mb.x, mb.y, ma.x, ma.y);
+            *reinterpret_cast<float4*>(prow + (ha - la - 1)) = make_float4(mb.x, mb.y, ma.x, ma.y);
           } else {
             *reinterpret_cast<float4*>(prow + la) = make_float4(aa.x, aa.y, ab.x, ab.y);
-            prow[half - la] = ma;
-            prow[half - la - 1] = mb;
+            prow[ha - la] = ma;
+            prow[ha - la - 1] = mb;
           }
         }
       }
@@ -582,14 +495,14 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       int4 rec_next = make_int4(0, 0, 0, 0);          // fp32: next entry's record loaded one iteration ahead
       if (sizeof(T) == 4 && nb + tid < ne) rec_next = __ldg(pp.noderec + nb + tid);
       for (int t = nb + tid; t < ne; t += nthr) {
-        int j, l, b1, b2;
+        int j, l, b1, b2, hj = half;
         T t1, t2;
         if constexpr (sizeof(T) == 4) {             // fp32: precomputed record (one 16-B load)
           const int4 rec = rec_next;
           if (t + nthr < ne) rec_next = __ldg(pp.noderec + t + nthr);
           b1 = int(short(rec.x & 0xFFFF)); b2 = rec.x >> 16;
           t1 = __int_as_float(rec.y); t2 = __int_as_float(rec.z);
-          j = int(uint32_t(rec.w) >> 16); l = rec.w & 0xFFFF;
+          j = (rec.w >> 16) & 0xFFF; l = rec.w & 0xFFFF; hj = half >> ((uint32_t(rec.w) >> 28) & 3);   // Pol slot
         } else {                                    // fp64: node coordinates in fp64 on the fly
           const uint32_t nd = __ldg(pp.nodes + t);
           j = int(nd >> 16); l = int(nd & 0xffffu);
@@ -599,7 +512,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           b1 = int(f1); b2 = int(f2);
           t1 = T(k1 - f1); t2 = T(k2 - f2);
         }
-        const bool pair = (l != 0) && (2 * l != half);
+        const bool pair = (l != 0) && (2 * l != hj);
         T wx[W], wy[W];
 #pragma unroll
         for (int q = 0; q < W; ++q) { wx[q] = phi(t1 - T(q)); wy[q] = phi(t2 - T(q)); }
@@ -620,7 +533,7 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           accB = rfma(wx[q], sb, accB);
         }
         Pol[(int64_t)j * half + l] = accA;
-        if (pair) Pol[(int64_t)j * half + (half - l)] = accB;
+        if (pair) Pol[(int64_t)j * half + (hj - l)] = accB;
       }
       __syncthreads();
       PROF_MARK(3);
@@ -660,8 +573,10 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           const int q = lane & 15;
           // ring j sampled at every s_j-th angle (plan.cpp): the unsampled positions of the half ring are zeros of
           // the stuffed sequence, never written by the gather and not loaded here
-          const int ma = __ldg(pp.ring_s + jg + jj) - 1, mb = two ? __ldg(pp.ring_s + jg + jj + 1) - 1 : 0;
-          // volatile: issued here (not sunk to the use a group later), completion tracked by the scoreboard
+          const int sa = __ldg(pp.ring_s + jg + jj), sb = two ? __ldg(pp.ring_s + jg + jj + 1) : 1;
+          const int ma = sa - 1, mb = sb - 1, la2 = 31 - __clz(sa), lb2 = 31 - __clz(sb);
+          // volatile: issued here (not sunk to the use a group later), completion tracked by the scoreboard.
+          // Sample t of the stuffed ring is slot t / s of the ring's contiguous samples (plan.cpp pol_slot)
 #pragma unroll
           for (int t1 = 0; t1 < 16; ++t1) {
             const int t = 16 * t1 + q;
@@ -669,9 +584,9 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
             pfb[t1] = 0.f;
             // predicated loads (no branches): @p ld, the register keeps its 0 otherwise
             asm volatile("{ .reg .pred p; setp.eq.s32 p, %2, 0; @p ld.global.f32 %0, [%1]; }"
-                         : "+f"(pfa[t1]) : "l"(fa + 2 * t), "r"(t & ma));
+                         : "+f"(pfa[t1]) : "l"(fa + 2 * (t >> la2)), "r"(t & ma));
             asm volatile("{ .reg .pred p; setp.eq.s32 p, %2, 0; @p ld.global.f32 %0, [%1]; }"
-                         : "+f"(pfb[t1]) : "l"(fb + 2 * t), "r"(two ? (t & mb) : 1));
+                         : "+f"(pfb[t1]) : "l"(fb + 2 * (t >> lb2)), "r"(two ? (t & mb) : 1));
           }
         }
       }
@@ -728,9 +643,11 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           const T2* fa = Pol + (int64_t)(j0 + jj) * half;
           const T2* fb = two ? fa + half : fa;
           // rings sampled at every s_j-th angle (reading Q21): the other positions are zeros of the stuffed ring
-          const int ma = __ldg(pp.ring_s + j0 + jj) - 1, mb = two ? __ldg(pp.ring_s + j0 + jj + 1) - 1 : 0;
-          auto ring_a = [&](int t) -> T2 { return (t & ma) ? T2{T(0), T(0)} : fa[t]; };
-          auto ring_b = [&](int t) -> T2 { return (two && !(t & mb)) ? fb[t] : T2{T(0), T(0)}; };
+          // (sample t of the stuffed ring = slot t / s of the ring's contiguous samples, plan.cpp pol_slot)
+          const int sa = __ldg(pp.ring_s + j0 + jj), sb = two ? __ldg(pp.ring_s + j0 + jj + 1) : 1;
+          const int ma = sa - 1, mb = sb - 1, la2 = 31 - __clz(sa), lb2 = 31 - __clz(sb);
+          auto ring_a = [&](int t) -> T2 { return (t & ma) ? T2{T(0), T(0)} : fa[t >> la2]; };
+          auto ring_b = [&](int t) -> T2 { return (two && !(t & mb)) ? fb[t >> lb2] : T2{T(0), T(0)}; };
           auto ldu = [&](int t) -> T2 { return T2{ring_a(t).x, ring_b(t).x}; };
           fft_ct<T2, MC, false, FG>(ldu, stR, myA, myB, twM, glane, gbar);
           gsync<FG>(gbar);

@@ -386,8 +386,7 @@ fbspca_status build_host_plan(Plan& P) {
     return (u2 + w <= last) ? p : -1;
   };
   const bool doubles = P.dt == FBSPCA_F32 && w == 6 && pow2_kernel && !getenv("FBSPCA_NO_DOUBLES");
-  std::vector<std::vector<std::array<int, 3>>> ph_single(phase_lo.size()), ph_double(phase_lo.size()),
-      ph_quad(phase_lo.size());
+  std::vector<std::vector<std::array<int, 3>>> ph_single(phase_lo.size()), ph_double(phase_lo.size());
   std::vector<uint32_t> singles;
   std::vector<std::array<uint32_t, 2>> dbl;
   // Angular stride per ring (fp32 compile-time ring-pair kernels: M in {64, 128, 256, 512, 600, 720}).  Ring j only feeds K4 blocks k <= kneed(j) = max{k : kj0[k] <= j},
@@ -416,48 +415,17 @@ fbspca_status build_host_plan(Plan& P) {
       P.ring_s[j] = sj;
     }
   }
-  // Quad entries (M = 256 fp32 kernel): pair leaders a = (j, l), b = (j, l + s), c = (j + 1, l), d = (j + 1, l + s) of
-  // two adjacent rings with the same stride s whose four anchors lie within kQuadW - w of each other in both directions
-  // share one kQuadW x kQuadW window at U = min anchors: 2 kQuadW^2 grid loads for the four direct nodes and their
-  // four mirrors (theta -> pi - theta): 12.25 loads per node at kQuadW = 7 against 24.5 for a double entry.  Each
-  // node's 6 x 6 taps sit at offsets (o1, o2) of the window; the kernel evaluates the window weights at all kQuadW
-  // positions and zeroes those outside the support.  Formed greedily along each even ring pair before the doubles
-  // (C3: 47 % of the pair leaders at kQuadW = 7, 97 % at 8).  FBSPCA_NO_QUADS=1 leaves everything to doubles / singles.
-  std::vector<std::array<uint32_t, 1>> quad;                 // (j << 16) | l of leader a
-  std::vector<char> in_quad(size_t(P.n_xi) * (half + 1), 0);
-  auto phase_of_quad = [&](int u2) {       // all w + 2 columns must be valid grid columns of the phase
-    const int p = (u2 - b2min) / (S - w + 1);
-    if (p >= (int)phase_lo.size()) return -1;
-    const int last = std::min(phase_lo[p] + S - 1, b2max + w - 1);
-    return (u2 + kQuadW - 1 <= last) ? p : -1;
+  auto pol_slot = [&](uint32_t nd) {
+    const int j = int(nd >> 16), l = int(nd & 0xffffu), sj = P.ring_s[j];
+    const int ls = sj == 8 ? 3 : sj == 4 ? 2 : sj == 2 ? 1 : 0;
+    return (uint32_t(j) << 16) | uint32_t(l >> ls) | (uint32_t(ls) << 28);
   };
-  const bool quads = doubles && hw16 && kQuadW >= w && !getenv("FBSPCA_NO_QUADS");
-  if (quads)
-    for (int j = 0; j + 1 < P.n_xi; j += 2) {
-      const int sj = P.ring_s[j];
-      if (P.ring_s[j + 1] != sj) continue;
-      for (int l = sj; 2 * (l + sj) < half;) {
-        const auto a = anchor(j, l), b = anchor(j, l + sj), c2 = anchor(j + 1, l), d = anchor(j + 1, l + sj);
-        const int lo1 = std::min({a.first, b.first, c2.first, d.first}), hi1 = std::max({a.first, b.first, c2.first, d.first});
-        const int lo2 = std::min({a.second, b.second, c2.second, d.second}), hi2 = std::max({a.second, b.second, c2.second, d.second});
-        const int p = phase_of_quad(lo2);
-        if (hi1 - lo1 <= kQuadW - w && hi2 - lo2 <= kQuadW - w && p >= 0) {
-          ph_quad[p].push_back({lo1, lo2, int(quad.size())});
-          quad.push_back({(uint32_t(j) << 16) | uint32_t(l)});
-          for (int dj = 0; dj < 2; ++dj)
-            for (int dl = 0; dl < 2; ++dl) in_quad[size_t(j + dj) * (half + 1) + l + dl * sj] = 1;
-          l += 2 * sj;
-        } else {
-          l += sj;
-        }
-      }
-    }
+  if (P.n_xi >= 4096) { set_error("n_xi >= 4096: polar node records hold 12-bit ring indices"); return FBSPCA_ERR_CONFIG; }
   for (int j = 0; j < P.n_xi; ++j) {
     const int sj = P.ring_s[j];               // ring j's angles theta_l, l = 0, sj, 2 sj, .. (sj | half/2)
     for (int l = 0; 2 * l <= half; l += sj) {
-      if (in_quad[size_t(j) * (half + 1) + l]) continue;
       const auto a = anchor(j, l);
-      if (doubles && l >= 1 && 2 * (l + sj) < half && !in_quad[size_t(j) * (half + 1) + l + sj]) {
+      if (doubles && l >= 1 && 2 * (l + sj) < half) {
         const auto b = anchor(j, l + sj);
         const int u1 = std::min(a.first, b.first), u2 = std::min(a.second, b.second);
         const int p = phase_of_double(u2);
@@ -519,36 +487,11 @@ fbspca_status build_host_plan(Plan& P) {
   }
   P.nodes.clear();
   P.dnoderec.clear();
-  P.qnoderec.clear();
   int np = 0;
   for (size_t p = 0; p < phase_lo.size(); ++p) {
     pp.phase_lo[np] = phase_lo[p];
     pp.phase_node_begin[np] = int(P.nodes.size());
     pp.phase_dbl_begin[np] = int(P.dnoderec.size() / 8);
-    pp.phase_quad_begin[np] = int(P.qnoderec.size() / 12);
-    for (uint32_t id : pack_gather_items(ph_quad[p], S)) {
-      // {U1 | U2 << 16, offsets (o1 | o2 << 2 in 4 bits per node) | s << 16, (j << 16) | l, 0}, {t1' of a, b, c, d},
-      // {t2' of a, b, c, d}: t' = k - U = (k - b) + o, the node's distance from the window's first row / column
-      const uint32_t nd = quad[id][0];
-      const int j = int(nd >> 16), l = int(nd & 0xffffu), sj = P.ring_s[j];
-      const int jj[4] = {j, j, j + 1, j + 1}, ll[4] = {l, l + sj, l, l + sj};
-      std::pair<int, int> an[4];
-      int u1 = 1 << 30, u2 = 1 << 30;
-      for (int i = 0; i < 4; ++i) { an[i] = anchor(jj[i], ll[i]); u1 = std::min(u1, an[i].first); u2 = std::min(u2, an[i].second); }
-      int32_t rec[12] = {0};
-      rec[0] = int32_t((uint32_t(u1) & 0xFFFFu) | (uint32_t(u2) << 16));
-      int of = 0;
-      for (int i = 0; i < 4; ++i) {
-        const int o1 = an[i].first - u1, o2 = an[i].second - u2;
-        of |= (o1 | (o2 << 2)) << (4 * i);
-        const float t1 = float(rho[jj[i]] * cs[2 * ll[i]] - u1), t2 = float(rho[jj[i]] * cs[2 * ll[i] + 1] - u2);
-        std::memcpy(&rec[4 + i], &t1, 4);
-        std::memcpy(&rec[8 + i], &t2, 4);
-      }
-      rec[1] = of | (sj << 16);
-      rec[2] = int32_t(nd);
-      P.qnoderec.insert(P.qnoderec.end(), rec, rec + 12);
-    }
     for (uint32_t id : pack_gather_items(ph_single[p], S)) P.nodes.push_back(singles[id]);
     for (uint32_t id : pack_gather_items(ph_double[p], S)) {
       // {U1 | U2 << 16, t1a, t2a, offsets}, {node a, t1b, t2b, node b}; t = k - b of each node's own anchor
@@ -562,14 +505,14 @@ fbspca_status build_host_plan(Plan& P) {
       rec[0] = int32_t((uint32_t(u1) & 0xFFFFu) | (uint32_t(u2) << 16));
       std::memcpy(&rec[1], &t1a, 4); std::memcpy(&rec[2], &t2a, 4);
       rec[3] = (aa.first - u1) | ((aa.second - u2) << 1) | ((ab.first - u1) << 2) | ((ab.second - u2) << 3);
-      rec[4] = int32_t(na);
+      rec[4] = int32_t(pol_slot(na));
       std::memcpy(&rec[5], &t1b, 4); std::memcpy(&rec[6], &t2b, 4);
-      rec[7] = int32_t(nb);
+      rec[7] = int32_t(pol_slot(nb));
       P.dnoderec.insert(P.dnoderec.end(), rec, rec + 8);
     }
     if (getenv("FBSPCA_DEBUG_PLAN"))
-      fprintf(stderr, "phase %d: lo %d, %zu single pair-leaders, %zu doubles, %zu quads\n", np, phase_lo[p],
-              ph_single[p].size(), ph_double[p].size(), ph_quad[p].size());
+      fprintf(stderr, "phase %d: lo %d, %zu single pair-leaders, %zu doubles\n", np, phase_lo[p],
+              ph_single[p].size(), ph_double[p].size());
     ++np;
   }
   pp.n_phase = np;
@@ -585,11 +528,14 @@ fbspca_status build_host_plan(Plan& P) {
   }
   pp.phase_node_begin[np] = int(P.nodes.size());
   pp.phase_dbl_begin[np] = int(P.dnoderec.size() / 8);
-  pp.phase_quad_begin[np] = int(P.qnoderec.size() / 12);
   P.rho = rho;
   P.cs = cs;
   // per-entry record for the fp32 gather: {b1 | b2 << 16, t1, t2, (j << 16) | l}, the same fp64 arithmetic
   // the fp64 kernel path performs on the fly (k = rho_j (cos, sin) theta_l, b = ceil(k - w/2), t = k - b)
+  // Pol slot of a node: ring j keeps its n_theta / s_j samples contiguous (sample l at l / s_j, mirrors at
+  // half_j - l / s_j, half_j = half / s_j), so the gather writes whole 32-byte sectors of the per-CTA polar scratch
+  // (partially written sectors made every ring load an L2 miss filled from DRAM).  Encoded (j << 16) | (l / s_j) |
+  // (log2 s_j << 28) in the fp32 records; j < 4096.
   P.noderec.resize(4 * P.nodes.size());
   for (size_t e = 0; e < P.nodes.size(); ++e) {
     const uint32_t nd = P.nodes[e];
@@ -602,7 +548,7 @@ fbspca_status build_host_plan(Plan& P) {
     rec[0] = int32_t((uint32_t(b1) & 0xFFFFu) | (uint32_t(b2) << 16));
     std::memcpy(&rec[1], &t1, 4);
     std::memcpy(&rec[2], &t2, 4);
-    rec[3] = int32_t(nd);
+    rec[3] = int32_t(pol_slot(nd));
     std::memcpy(&P.noderec[4 * e], rec, 16);
   }
   return FBSPCA_OK;
