@@ -129,7 +129,7 @@ PAPER_IMG_S = {"T3": (1e5 / (1438.0 + 42.0), "P:490-492: 1,438 s expansion + 42 
 
 def cpu_baseline(cfg, seconds_target=15.0):
     """The oracle as it stands (expansion + covariance) on a bounded sample of the same workload: the sample grows
-    until it takes about seconds_target of host time (at most 1,024 images, three sizings)."""
+    until it takes about seconds_target of host time (at most 2,048 images, three sizings)."""
     import numpy as np
     import oracle as O
     import synth
@@ -142,9 +142,9 @@ def cpu_baseline(cfg, seconds_target=15.0):
         t0 = time.perf_counter()
         O.block_covariance(O.expand(imgs, basis))
         dt = time.perf_counter() - t0
-        if dt >= 0.5 * seconds_target or m >= 1024:
+        if dt >= 0.5 * seconds_target or m >= 2048:
             break
-        m = max(m + 1, min(1024, int(m * seconds_target / max(dt, 1e-3))))
+        m = max(m + 1, min(2048, int(m * seconds_target / max(dt, 1e-3))))
     return {"value": m / dt, "unit": "images/s", "cores": torch.get_num_threads(), "host_cpus": os.cpu_count(),
             "kind": "oracle",
             "sample": f"first {m} images of {cfg['name']} (oracle: direct Fourier sum + FFT + GL + fp64 covariance), "

@@ -1,12 +1,23 @@
 """Per-region totals of an ncu source page (--print-source cuda,sass --csv): SASS rows are put in address order and
 each is assigned to the region of the most recent kernels_polar.cu line at or before it (inlined helpers from
-other files inherit the caller's region).  usage: python tools/ncu_regions.py mix.csv n_images"""
+other files inherit the caller's region; region starts are located from marker comments in kernels_polar.cu).
+usage: python tools/ncu_regions.py mix.csv n_images"""
 import csv
 import sys
 
-REGIONS = [  # (first kernels_polar.cu line, name) -- kernels_polar.cu as of round 2
-    (0, "setup"), (160, "image/row FFT"), (208, "col fill"), (228, "col FFT"), (246, "gather doubles"),
-    (370, "gather singles"), (420, "ring FFT"), (600, "write-out"), (650, "tail")]
+def _find_regions():
+    src = open("/root/repo/paper_1412_0781_b200/csrc/kernels_polar.cu").read().splitlines()
+    marks = [("K1a: row FFTs", "image/row FFT"), ("per phase: K1b column FFTs", "col fill"), ("PROF_MARK(1);", "col FFT"),
+             ("if constexpr (sizeof(T) == 4 && W == 6 && MC > 0)", "gather doubles"),
+             ("const int nb = pp.phase_node_begin[ph]", "gather singles"), ("const bool want_prefetch", "ring FFT"),
+             ("const int64_t kstride = pp.ghat_kstride", "write-out"), ("PROF_STORE();", "tail")]
+    out = [(0, "setup")]
+    for pat, name in marks:
+        ln = next(i + 1 for i, l in enumerate(src) if pat in l and i + 1 > out[-1][0])
+        out.append((ln, name))
+    return out
+REGIONS = _find_regions()
+KSTART = next(i + 1 for i, l in enumerate(open("/root/repo/paper_1412_0781_b200/csrc/kernels_polar.cu").read().splitlines()) if l.startswith("polar_kernel("))
 
 
 def region_of(line):
@@ -50,7 +61,7 @@ sass.sort()
 agg = {}
 last_polar = 0
 for addr, (p, ln), inst, wf, smp, st in sass:
-    if p == "kernels_polar.cu" and ln >= 80:       # helpers above the kernel body inherit the caller's region
+    if p == "kernels_polar.cu" and ln >= KSTART:       # helpers above the kernel body inherit the caller's region
         last_polar = ln
     reg = region_of(last_polar)
     a = agg.setdefault(reg, {"inst": 0, "wf": 0, "smp": 0, "st": {}})
