@@ -16,10 +16,14 @@ constexpr int kMaxPhases = 64;
 constexpr int kCovChunk = 1024;         // images per SIMT covariance split-K chunk (bounds fp32 accumulation length)
 constexpr int kCovBatch = 16384;        // images per SIMT covariance launch
 constexpr int kCovChunkTc = 4096;       // images per tensor-core split-K chunk (cov_tma_chunk() <= this)
-constexpr int kCovBatchTc = 65536;      // images per tensor-core covariance launch (A/B on B200: 16384 -> 65536 took the
-                                        // C3 K5 from 2.03 to 1.85 ms: more items per persistent CTA, fewer launch tails)
-constexpr int kCovMaxChunks = kCovBatch / kCovChunk;        // 16 scratch slots; kCovBatchTc / kCovChunkTc = 16 too
-static_assert(kCovBatchTc / kCovChunkTc <= kCovMaxChunks, "covariance scratch slots");
+#ifndef FBSPCA_COV_SLOTS
+#define FBSPCA_COV_SLOTS 32
+#endif
+constexpr int kCovMaxChunks = FBSPCA_COV_SLOTS;              // split-K scratch slots (SIMT: kCovBatch / kCovChunk = 16)
+static_assert(kCovBatch / kCovChunk <= kCovMaxChunks, "covariance scratch slots");
+constexpr int kCovBatchTc = kCovChunkTc * kCovMaxChunks;     // images per tensor-core covariance launch: 131,072, so a
+                                        // C3 step (100,000 images) is one launch (16,384 -> 65,536 took the C3 K5 from
+                                        // 2.03 to 1.85 ms: more items per persistent CTA, fewer launch tails)
 constexpr int kCovChunk0 = 128;         // images per k = 0 fp64 CTA (tensor-core path: its own scratch, more CTAs)
 constexpr int kCovMaxSub0 = kCovBatchTc / kCovChunk0;
 
