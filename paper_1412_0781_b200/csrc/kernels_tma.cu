@@ -332,6 +332,10 @@ radial_tma_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constan
 // so that S[q][q'] = acc_q[q'] + acc_q'[q] (q < q'), S[q][q] = acc_q[q].  The item's S goes to scratch[chunk] as the
 // fp64 upper triangle (combined through shared memory); cov_reduce_kernel adds the chunks in fixed order.
 constexpr int K5_CK = 4;
+#ifndef FBSPCA_K5_TH
+#define FBSPCA_K5_TH 32
+#endif
+template <int RR> constexpr int K5_TH = RR < FBSPCA_K5_TH ? RR : FBSPCA_K5_TH;   // epilogue transpose pass width
 struct K5Args {
   int k_max, nchunk, chunk, drain, stages, rmax, ck;              // ck: K chunks per stage (<= K5_CK)
   int k_lo;                                                       // first k of this launch (k_lo..k_max)
@@ -360,8 +364,9 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
   constexpr int AW = TROWS;                                         // accumulator columns (N of a stacked tile)
   const uint32_t tile_bytes = uint32_t(TROWS) * ROWB;
   const uint32_t stage_bytes = CK * tile_bytes;
-  float* tr = reinterpret_cast<float*>(sm + NS * stage_bytes);      // RR x (RR + 1) epilogue transpose
-  uint64_t* full = reinterpret_cast<uint64_t*>(tr + RR * (RR + 1));
+  constexpr int TH = K5_TH<RR>;                                     // epilogue transpose: column passes of TH
+  float* tr = reinterpret_cast<float*>(sm + NS * stage_bytes);      // RR x (TH + 1)
+  uint64_t* full = reinterpret_cast<uint64_t*>(tr + RR * (TH + 1));
   uint64_t* loready = full + NS;
   uint64_t* empty = loready + NS;
   uint64_t* accfull = empty + NS;                                   // 2
@@ -537,23 +542,42 @@ cov_tma_kernel(const __grid_constant__ MapSet tm_a, const K5Args args) {
       }
     }
     drain(pending);
-    // S = acc_q[q'] + acc_q'[q] through shared memory (summing the G stacked groups), fp64 upper triangle
-    for (int gg = 0; gg < e.G; ++gg) {
-      named_sync(1, 128);
-      if (gw == gg && qq < b && qq < RR) {
+    // S = acc_q[q'] + acc_q'[q] (summing the G stacked groups) as the fp64 upper triangle, through shared memory in
+    // column passes of TH (tr holds A[r][h0 .. h0 + TH) of every row r, A = the group-summed acc rows: a third of the
+    // full RR x (RR + 1) transpose, so a 2-CTA RR = 64 CTA fits three 32 KB stages).  Element (r, c), r < c: written
+    // as double(A[c][r]) in r's pass when c lies in a later pass, += double(A[r][c]) in c's pass (the same fp64 sum
+    // as in one pass; bar.sync orders the CTA's global accesses); both in one pass: written at once.
+    double* dst = args.scratch + int64_t(ch) * args.scratch_stride + args.blk_off[k];
 #pragma unroll
-        for (int c = 0; c < RR; ++c) {
-          if (gg == 0) tr[qq * (RR + 1) + c] = acc[c];
-          else tr[qq * (RR + 1) + c] += acc[c];
+    for (int h0 = 0; h0 < RR; h0 += TH) {
+      if (h0 < b) {
+        for (int gg = 0; gg < e.G; ++gg) {
+          named_sync(1, 128);
+          if (gw == gg && qq < b) {
+#pragma unroll
+            for (int c = 0; c < TH; ++c) {
+              if (gg == 0) tr[qq * (TH + 1) + c] = acc[h0 + c];
+              else tr[qq * (TH + 1) + c] += acc[h0 + c];
+            }
+          }
+        }
+        named_sync(1, 128);
+        const int h1 = h0 + TH;
+        for (int r = warp; r < min(pk, h1); r += 4) {        // row r of the packed upper triangle: warp-wide
+          double* drow = dst + (int64_t)r * pk - (int64_t)r * (r - 1) / 2;
+          const bool rin = r >= h0;
+          for (int c = max(r, h0) + lane; c < pk; c += 32) {
+            const bool cin = c < h1;                           // c >= h0 here
+            if (rin && cin)
+              drow[c - r] = c == r ? double(tr[r * (TH + 1) + (r - h0)])
+                                   : double(tr[r * (TH + 1) + (c - h0)]) + double(tr[c * (TH + 1) + (r - h0)]);
+            else if (rin)                                      // c in a later pass: A[c][r] now
+              drow[c - r] = double(tr[c * (TH + 1) + (r - h0)]);
+            else if (cin)                                      // r in an earlier pass: + A[r][c]
+              drow[c - r] += double(tr[r * (TH + 1) + (c - h0)]);
+          }
         }
       }
-    }
-    named_sync(1, 128);
-    double* dst = args.scratch + int64_t(ch) * args.scratch_stride + args.blk_off[k];
-    for (int r = warp; r < pk; r += 4) {                     // row r of the packed upper triangle: warp-wide
-      double* drow = dst + (int64_t)r * pk - (int64_t)r * (r - 1) / 2;
-      for (int c = r + lane; c < pk; c += 32)
-        drow[c - r] = c == r ? double(tr[r * (RR + 1) + r]) : double(tr[r * (RR + 1) + c]) + double(tr[c * (RR + 1) + r]);
     }
   }
   named_sync(1, 128);
@@ -810,9 +834,9 @@ cudaError_t launch_radial_tma(const Plan& P, int64_t nb, int64_t i0, int64_t ld,
 
 template <int RR>
 static cudaError_t launch_cov_tma_t(const Plan& P, const MapSet& ta, K5Args& a, cudaStream_t s) {
-  const int fixed = RR * (RR + 1) * 4 + 1024 + 256;
+  const int fixed = RR * (K5_TH<RR> + 1) * 4 + 1024 + 256;
   const char* env = getenv("FBSPCA_K5_CTAS");
-  const int per_sm = env ? std::max(1, std::min(2, atoi(env))) : 2;
+  const int per_sm = env ? std::max(1, std::min(2, atoi(env))) : (RR <= 64 ? 2 : 1);   // RR = 128: 255 registers
   const int budget = (per_sm == 2 ? 113 : 227) * 1024;
   a.ck = K5_CK;                                            // fewer chunks per stage when a tile is 32 KB
   if (const char* e = getenv("FBSPCA_K5_CK")) a.ck = std::max(1, std::min(8, atoi(e)));   // A/B knob
