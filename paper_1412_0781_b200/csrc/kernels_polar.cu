@@ -492,9 +492,17 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
         }
       }
       const int nb = pp.phase_node_begin[ph], ne = pp.phase_node_begin[ph + 1];
+      // singles are dealt from the last thread down: the threads the double entries' ragged last round left idle
+      // take them first (C3 phase 1: 2072 doubles = 4 x 512 + 24, 272 singles -- no thread does both a fifth
+      // double and a single).  A reversed 16-aligned half-warp is the same half-warp: the bank packing holds.
+#ifdef FBSPCA_SINGLES_FWD
+      const int rtid = tid;                           // A/B: the forward deal
+#else
+      const int rtid = nthr - 1 - tid;
+#endif
       int4 rec_next = make_int4(0, 0, 0, 0);          // fp32: next entry's record loaded one iteration ahead
-      if (sizeof(T) == 4 && nb + tid < ne) rec_next = __ldg(pp.noderec + nb + tid);
-      for (int t = nb + tid; t < ne; t += nthr) {
+      if (sizeof(T) == 4 && nb + rtid < ne) rec_next = __ldg(pp.noderec + nb + rtid);
+      for (int t = nb + rtid; t < ne; t += nthr) {
         int j, l, b1, b2, hj = half;
         T t1, t2;
         if constexpr (sizeof(T) == 4) {             // fp32: precomputed record (one 16-B load)
