@@ -23,6 +23,9 @@ sys.path.insert(0, ROOT)
 
 BATCH = 50000         # images per expand batch (ghat workspace 9.4 GB at C3); 2 batches per 100k step
                       # (A/B on B200: 25000 -> 50000 took the polar kernel from 54.7 to 54.4 ms: fewer launch tails)
+EPS = 1e-4            # fbspca_plan's NUFFT tolerance for the bench: north_star's coefficient tolerance (rel l2 <= 1e-4
+                      # per image).  At C3 it selects the w = 5 window (measured 5.9e-5 max per image against the fp64
+                      # oracle; --eps 1e-5, the library default, runs w = 6: 5.7e-6).  DESIGN.md Q16 / section 9.
 METRIC = "images/sec (expansion+covariance, L=128) at 1/2/4/8 B200; % HBM roofline"
 
 
@@ -39,6 +42,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nccl", action="store_true",
                     help="use the NCCL communicator path even on one GPU (the world > 1 code path, 1 rank)")
+    ap.add_argument("--eps", type=float, default=EPS, help="fbspca_plan's NUFFT tolerance (window width w)")
     ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay measurement")
     return ap.parse_args()
 
@@ -214,11 +218,11 @@ def main():
     n_local = e - s
     dt = F.F32 if cfg["dtype"] == "f32" else F.F64
     # expand batch: args.batch, capped so the plan's ghat workspace stays <= 40 GB (C5: ~25,800 images)
-    probe = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], dtype=dt, device=-1)
+    probe = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], eps=args.eps, dtype=dt, device=-1)
     ghat_per_image = (probe.k_max + 1) * 2 * probe.n_xi * (4 if dt == F.F32 else 8)
     batch = max(1, min(args.batch, int(40e9 // ghat_per_image)))
     del probe
-    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], dtype=dt, device=local, max_batch=batch)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], eps=args.eps, dtype=dt, device=local, max_batch=batch)
     plan.bench_batch = batch
     comm = None
     if world > 1 or args.nccl:
@@ -405,7 +409,7 @@ def main():
             "config": {"workload": (f"{cfg['name']}: BASELINE.json configs[{int(cfg['name'][1]) - 1}]"
                                     if cfg["name"].startswith("C") else WORKLOADS[cfg["name"]]), "n": n,
                        "L": cfg["L"], "R": cfg["R"], "c": cfg["c"], "parallelism": f"dp{world}",
-                       "n_per_rank": n_local, "eps": 1e-5, "M": plan.M, "w": plan.w, "expand_batch": plan_batch(plan),
+                       "n_per_rank": n_local, "eps": args.eps, "M": plan.M, "w": plan.w, "expand_batch": plan_batch(plan),
                        "l2": f"inputs larger than L2 ({n * cfg['L'] * cfg['L'] * (4 if dt == F.F32 else 8) / 1e9:.1f} GB "
                              "of images read per step, L2 126 MB)"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",

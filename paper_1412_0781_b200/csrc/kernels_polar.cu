@@ -418,8 +418,9 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
       }
       __syncthreads();
       PROF_MARK(2);
-      if constexpr (sizeof(T) == 4 && W == 6 && MC > 0) {
-        // double entries: nodes a, b of one ring (+ their mirrors) over one shared 7 x 7 window at U
+      if constexpr (sizeof(T) == 4 && (W == 5 || W == 6) && MC > 0) {
+        constexpr int W1 = W + 1;                     // the shared (W + 1) x (W + 1) window
+        // double entries: nodes a, b of one ring (+ their mirrors) over one shared (W + 1) x (W + 1) window at U
         const int db = pp.phase_dbl_begin[ph], de = pp.phase_dbl_begin[ph + 1];
         // records are loaded one iteration ahead (an L2 round trip per entry was the loop's top stall)
         int4 n0 = make_int4(0, 0, 0, 0), n1 = n0;
@@ -430,37 +431,37 @@ polar_kernel(const PolarParams* __restrict__ ppg, const T* __restrict__ images, 
           const int u1 = int(short(r0.x & 0xFFFF)), u2 = r0.x >> 16, of = r0.w;
           const float t1a = __int_as_float(r0.y), t2a = __int_as_float(r0.z);
           const float t1b = __int_as_float(r1.y), t2b = __int_as_float(r1.z);
-          float xa[7], ya[7], xb[7], yb[7];
+          float xa[W1], ya[W1], xb[W1], yb[W1];
           {
-            float wa[6], va[6], wb[6], vb[6];
+            float wa[W], va[W], wb[W], vb[W];
 #pragma unroll
-            for (int q = 0; q < 6; ++q) {               // nodes a and b in one f32x2 pair per direction
+            for (int q = 0; q < W; ++q) {               // nodes a and b in one f32x2 pair per direction
               phi.pair(t1a, t1b, float(q), wa[q], wb[q]);
               phi.pair(t2a, t2b, float(q), va[q], vb[q]);
             }
             const bool o1a = of & 1, o2a = of & 2, o1b = of & 4, o2b = of & 8;
 #pragma unroll
-            for (int r = 0; r < 7; ++r) {
-              xa[r] = o1a ? (r ? wa[r - 1] : 0.f) : (r < 6 ? wa[r] : 0.f);
-              ya[r] = o2a ? (r ? va[r - 1] : 0.f) : (r < 6 ? va[r] : 0.f);
-              xb[r] = o1b ? (r ? wb[r - 1] : 0.f) : (r < 6 ? wb[r] : 0.f);
-              yb[r] = o2b ? (r ? vb[r - 1] : 0.f) : (r < 6 ? vb[r] : 0.f);
+            for (int r = 0; r < W1; ++r) {
+              xa[r] = o1a ? (r ? wa[r - 1] : 0.f) : (r < W ? wa[r] : 0.f);
+              ya[r] = o2a ? (r ? va[r - 1] : 0.f) : (r < W ? va[r] : 0.f);
+              xb[r] = o1b ? (r ? wb[r - 1] : 0.f) : (r < W ? wb[r] : 0.f);
+              yb[r] = o2b ? (r ? vb[r - 1] : 0.f) : (r < W ? vb[r] : 0.f);
             }
           }
           const T2* gcol = Gc + (u2 - lo);
           T2 aa = T2{0.f, 0.f}, ab = aa, ma = aa, mb = aa;      // (node a, node b) x (direct, mirrored)
 #pragma unroll
-          for (int r = 0; r < 7; ++r) {
+          for (int r = 0; r < W1; ++r) {
             const T2* ga = gcol + (size_t)(u1 + r + row0) * S;
             const T2* gm = gcol + (size_t)(row0 - u1 - r) * S;
             T2 sa = T2{0.f, 0.f}, sb = sa, na = sa, nb2 = sa;
 #pragma unroll
-            for (int c = 0; c < 7; ++c) {
+            for (int c = 0; c < W1; ++c) {
               const T2 g = ga[c];
               sa = rfma(ya[c], g, sa); sb = rfma(yb[c], g, sb);
             }
 #pragma unroll
-            for (int c = 0; c < 7; ++c) {
+            for (int c = 0; c < W1; ++c) {
               const T2 g = gm[c];
               na = rfma(ya[c], g, na); nb2 = rfma(yb[c], g, nb2);
             }
@@ -826,7 +827,7 @@ cudaError_t launch_polar_t(const Plan& P, const void* d_images, int64_t n_img, i
 #define FBSPCA_POLAR_EXTERN(T, W, MC) \
   extern template cudaError_t launch_polar_t<T, W, MC>(const Plan&, const void*, int64_t, int64_t, cudaStream_t);
 #define FBSPCA_POLAR_LIST(X, P1, P2, P3, P4, P5, P6) \
-  P1(X(float, 6, 256)) P2(X(float, 6, 512)) P2(X(float, 6, 128)) P3(X(float, 6, 0)) P4(X(float, 7, 0)) P5(X(double, 13, 0)) P5(X(double, 13, 64)) P6(X(float, 6, 600)) P6(X(float, 6, 720))
+  P1(X(float, 6, 256)) P4(X(float, 5, 256)) P2(X(float, 6, 512)) P2(X(float, 6, 128)) P3(X(float, 6, 0)) P4(X(float, 7, 0)) P5(X(double, 13, 0)) P5(X(double, 13, 64)) P6(X(float, 6, 600)) P6(X(float, 6, 720))
 #define FBSPCA_ON(x) x
 #define FBSPCA_OFF(x)
 #if FBSPCA_POLAR_HERE(1)
@@ -875,6 +876,7 @@ cudaError_t launch_polar(const Plan& P, const void* d_images, int64_t n_img, int
     if (pow2 && P.M == 64) return launch_polar_t<double, 13, 64>(P, d_images, n_img, stride, s);
     return launch_polar_t<double, 13, 0>(P, d_images, n_img, stride, s);
   }
+  if (P.w == 5 && pow2 && P.M == 256) return launch_polar_t<float, 5, 256>(P, d_images, n_img, stride, s);   // eps >= 1e-4
   if (P.w == 6 && pow2) {
     switch (P.M) {
       case 128: return launch_polar_t<float, 6, 128>(P, d_images, n_img, stride, s);

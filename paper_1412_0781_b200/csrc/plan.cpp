@@ -273,7 +273,12 @@ fbspca_status build_host_plan(Plan& P) {
   while (!smooth5(M) || M % 2) ++M;
   P.M = M;
   int w = int(std::ceil(-std::log10(P.eps) - 1e-9)) + 1;         // error ~ 10^{-(w-1)} at sigma = 2
-  if (P.dt == FBSPCA_F32) { w = std::max(6, std::min(w, 7)); }   // eps >= 1e-6 (fp32 floor) -> w <= 7
+  // fp32: eps >= 1e-6 (the fp32 floor) -> w <= 7; eps >= 1e-4 -> w = 5 where a W = 5 kernel is compiled (M = 256 with
+  // n_theta = 2 M: the L = 128, c = 1/2 shape), else 6
+  if (P.dt == FBSPCA_F32) {
+    const int wmin = (M == 256 && P.n_theta == 2 * M && !getenv("FBSPCA_NO_W5")) ? 5 : 6;
+    w = std::max(wmin, std::min(w, 7));
+  }
   else { w = std::max(w, 13); if (w > 13) w = 13; }
   P.w = w;
   P.beta = 2.30 * w;
@@ -319,7 +324,7 @@ fbspca_status build_host_plan(Plan& P) {
   if (const char* e = getenv("FBSPCA_FFT_WARPS")) pp.fft_warps = std::max(1, std::min(16, atoi(e)));
   // the compile-time M = 256 fp32 kernel runs every FFT as half-warp radix-16 x 16 transforms (two per warp) with
   // its own per-warp scratch, on all 16 warps (one ring pair per warp per 32-ring group)
-  const bool hw16 = P.dt == FBSPCA_F32 && w == 6 && M == 256 && P.n_theta == 2 * M;
+  const bool hw16 = P.dt == FBSPCA_F32 && (w == 5 || w == 6) && M == 256 && P.n_theta == 2 * M;
   if (hw16) pp.fft_warps = 16;
   const int fixed = polar_fixed_smem(M, P.n_theta, L, csz, pp.fft_warps, P.k_max + 1, hw16);
   const int budget = cap - fixed;
@@ -385,7 +390,7 @@ fbspca_status build_host_plan(Plan& P) {
     const int last = std::min(phase_lo[p] + S - 1, b2max + w - 1);
     return (u2 + w <= last) ? p : -1;
   };
-  const bool doubles = P.dt == FBSPCA_F32 && w == 6 && pow2_kernel && !getenv("FBSPCA_NO_DOUBLES");
+  const bool doubles = P.dt == FBSPCA_F32 && (w == 5 || w == 6) && pow2_kernel && !getenv("FBSPCA_NO_DOUBLES");
   std::vector<std::vector<std::array<int, 3>>> ph_single(phase_lo.size()), ph_double(phase_lo.size());
   std::vector<uint32_t> singles;
   std::vector<std::array<uint32_t, 2>> dbl;
@@ -399,7 +404,7 @@ fbspca_status build_host_plan(Plan& P) {
   // 2 pi s_j / n_theta is the table's 2 pi / n_theta times the power of two s_j (capi.cu upload).  Inner rings need
   // far fewer angles: C3 gathers 0.70 of the nodes.  FBSPCA_NO_RING_STRIDE=1 samples every ring at all n_theta angles.
   P.ring_s.assign(P.n_xi, 1);
-  const bool ring_stride_kernel = P.dt == FBSPCA_F32 && w == 6 && pow2_kernel && P.n_theta == 2 * M;
+  const bool ring_stride_kernel = P.dt == FBSPCA_F32 && (w == 5 || w == 6) && pow2_kernel && P.n_theta == 2 * M;
   if (ring_stride_kernel && !getenv("FBSPCA_NO_RING_STRIDE")) {
     const double rc = std::sqrt(2.0) * std::ceil(0.5 * L);
     for (int j = 0; j < P.n_xi; ++j) {
@@ -519,7 +524,7 @@ fbspca_status build_host_plan(Plan& P) {
   // TMEM parking of the second phase's columns (kernels_polar.cu): M = 256 compile-time kernel with 16 FFT warps and two
   // phases; the warp's four row pairs x ng 32-column groups x 4 floats fit 64 TMEM columns (4 warps per lane quarter)
   pp.tmem_x = 0;
-  if (M == 256 && P.n_theta == 2 * M && P.dt == FBSPCA_F32 && w == 6 && pp.fft_warps == 16 && np == 2 &&
+  if (M == 256 && P.n_theta == 2 * M && P.dt == FBSPCA_F32 && (w == 5 || w == 6) && pp.fft_warps == 16 && np == 2 &&
       (L + 1) / 2 <= 4 * 16 && !getenv("FBSPCA_NO_TMEM_X")) {
     const int c1 = pp.phase_lo[1] - pp.col_lo;               // first row-pass column index of phase 1
     pp.tmem_g0 = c1 / 32;

@@ -32,7 +32,10 @@ DEV = torch.device("cuda:0") if torch.cuda.is_available() else None
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 TOL32 = 1e-4
-BENCH_BATCH = 50000                       # bench.py BATCH: images per expand batch in the timed configuration
+sys.path.insert(0, ROOT)
+from bench import BATCH as BENCH_BATCH, EPS as BENCH_EPS   # noqa: E402  (bench.py's timed configuration: images per
+                                                           # expand batch, fbspca_plan eps -- imported, not retyped)
+C3_EPS = sorted({BENCH_EPS, 1e-5, 1e-4})                   # the bench's plan, the library default (w = 6), w = 5
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -119,13 +122,15 @@ def test_c2_full_size_spectral_vs_cached_oracle():
 
 
 # ------------------------------------------------------------------ C3 full size, bench launch configuration
-@pytest.fixture(scope="module")
-def c3_run():
+@pytest.fixture(scope="module", params=C3_EPS, ids=lambda e: f"eps{e:g}")
+def c3_run(request):
+    eps = request.param
     cfg = synth.config("C3")
     n = cfg["n"]
     sig = synth.blobs.noise_sigma(cfg)                 # CPU, as bench.py's generator value up to rounding
     imgs = synth.blob_images(cfg, 0, n, device=DEV, sigma_n=sig)
-    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=BENCH_BATCH)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], eps=eps, device=0, max_batch=BENCH_BATCH)
+    assert plan.w == (5 if eps >= 1e-4 else 6)
     coeffs = torch.empty((plan.n_coef, n), dtype=plan.complex_dtype, device=DEV)
     blocks = torch.empty(plan.n_blk, dtype=torch.float64, device=DEV)
     mean = torch.empty(int(plan.p[0]), dtype=torch.float64, device=DEV)
@@ -169,7 +174,7 @@ def test_c3_sampled_coefficients_bench_config(c3_run):
     ref = O.to_flat(O.expand(r["imgs"][it].double().cpu().numpy(), basis))
     got = r["coeffs"][:, it].cpu().numpy().astype(np.complex128)
     rel = rel_l2_per_image(got, ref, basis)
-    print(f"C3 2048 sampled images: max rel l2 {rel.max():.3e}, median {np.median(rel):.3e}")
+    print(f"C3 (w = {r['plan'].w}) 2048 sampled images: max rel l2 {rel.max():.3e}, median {np.median(rel):.3e}")
     assert rel.max() <= TOL32, f"max per-image rel l2 {rel.max():.3e} at image {idx[rel.argmax()]}"
     assert np.all(got[: basis.p[0]].imag == 0)                                     # Q8
 
@@ -260,14 +265,16 @@ def test_eigenimages_parity():
 
 
 # ------------------------------------------------------------------ kernel instances + the eps contract
-@pytest.mark.parametrize("name,n,eps", [("C2", 40, 1e-6), ("C3", 8, 1e-6), ("C2", 40, 1e-5), ("C3", 8, 1e-4)])
+@pytest.mark.parametrize("name,n,eps", [("C2", 40, 1e-6), ("C3", 8, 1e-6), ("C2", 40, 1e-5), ("C3", 8, 1e-4),
+                                          ("C3", 150, 1e-3), ("C2", 40, 1e-4)])
 def test_eps_contract_fp32(name, n, eps):
-    """fbspca_plan's eps: w = ceil(log10(1/eps)) + 1 taps (fp32: clamped to [6, 7]); eps = 1e-6 selects the w = 7
-    runtime-radix polar kernel.  Contract (include/fbspca.h): per-image coefficient rel l2 <= max(4 eps, 4e-6)."""
+    """fbspca_plan's eps: w = ceil(log10(1/eps)) + 1 taps (fp32: clamped to [6, 7], and [5, 7] on the M = 256 kernel
+    -- C3's shape -- which has a w = 5 instance for eps >= 1e-4); eps = 1e-6 selects the w = 7 runtime-radix polar
+    kernel.  Contract (include/fbspca.h): per-image coefficient rel l2 <= max(4 eps, 4e-6)."""
     cfg = synth.config(name)
     imgs = synth.blob_images(cfg, 0, n, device=DEV)
     plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], eps=eps, device=0, max_batch=64)
-    assert plan.w == (7 if eps <= 1e-6 else 6)
+    assert plan.w == (7 if eps <= 1e-6 else 5 if (eps >= 1e-4 and name == "C3") else 6)
     got = F.fbspca_expand(plan, imgs).cpu().numpy().astype(np.complex128)
     basis = O.build_basis(cfg["c"], cfg["R"])
     ref = O.to_flat(O.expand(imgs.double().cpu().numpy(), basis))
