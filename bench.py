@@ -382,8 +382,10 @@ def main():
                 d["alg_gbs"] = wk["cov_bytes"] * n_local / (tms / 1e3) / 1e9
                 d["hbm_frac"] = d["alg_gbs"] / hbm
             kernels[name] = d
+        # committed ncu capture of the kernels this run launched: the polar kernel's w = 5 or w = 6 instance
+        traffic_file = "r2_ncu_traffic.json" if plan.w == 5 else "r2_ncu_traffic_eps1e-5.json"
         try:                                  # tensor-pipe activity of K4/K5 from the committed ncu capture (C3)
-            tjk = json.load(open(os.path.join(ROOT, "profiles", "r2_ncu_traffic.json")))["kernels"]
+            tjk = json.load(open(os.path.join(ROOT, "profiles", traffic_file)))["kernels"]
             if cfg["name"] == "C3":
                 for nm in ("radial_K4", "cov_K5"):
                     if nm in kernels:
@@ -395,7 +397,7 @@ def main():
         traffic = None                       # DRAM bytes per polar launch, from the committed ncu capture
         l1_busy = None
         try:
-            tj = json.load(open(os.path.join(ROOT, "profiles", "r2_ncu_traffic.json")))
+            tj = json.load(open(os.path.join(ROOT, "profiles", traffic_file)))
             if cfg["name"] == "C3":
                 traffic = tj["kernels"]["polar_K1K2K3"]["dram_bytes_per_image"] * imgs_per_launch
                 l1_busy = tj["kernels"]["polar_K1K2K3"]["l1_data_pipe_busy_frac"]
@@ -414,9 +416,9 @@ def main():
                              "of images read per step, L2 126 MB)"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
                          "frac": achieved / alu_peak, "traffic": traffic, "kernel": "polar_K1K2K3",
-                         "traffic_source": "profiles/r2_ncu_traffic.json (ncu dram bytes per image x images per launch)",
+                         "traffic_source": f"profiles/{traffic_file} (ncu dram bytes per image x images per launch)",
                          "binding_resource": {"name": "L1 / shared-memory data pipe (LSU wavefronts)", "busy_frac": l1_busy,
-                                              "source": "profiles/r2_ncu_traffic.json (ncu l1tex__data_pipe_lsu_wavefronts)"},
+                                              "source": f"profiles/{traffic_file} (ncu l1tex__data_pipe_lsu_wavefronts)"},
                          "algorithmic_bytes_per_launch": wk["polar_bytes"] * imgs_per_launch,
                          "peak_source": f"148 SM x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz (guide unit counts, "
                                         "MEASURED_PEAKS sm_max_mhz)",

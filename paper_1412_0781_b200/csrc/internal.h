@@ -197,6 +197,12 @@ fbspca_status estimate_params(int L, fbspca_dtype dt, int device, const void* d_
 cudaError_t launch_project(const Plan& P, const void* d_coeffs, int64_t n, const double* d_mean,
                            const double* d_evals, const double* d_evecs, double sigma2, int mode,
                            int64_t n_total, void* d_out, cudaStream_t s);
+// fp32 plans served by a compile-time-FFT polar kernel (launch_polar's dispatch; the plan emits double entries and
+// ring strides only for these -- the runtime-radix kernel gathers single entries on full rings).  Window widths
+// w = 5 (eps >= 1e-4) and w = 6 are compiled for every such M.
+inline bool polar_f32_ct_kernel(int M, int n_theta) {
+  return n_theta == 2 * M && (M == 128 || M == 256 || M == 512 || M == 600 || M == 720);
+}
 int polar_max_smem();
 cudaError_t launch_radial_tma(const Plan& P, int64_t nb, int64_t i0, int64_t ld, void* d_coeffs, cudaStream_t s);
 cudaError_t launch_cov_tma(const Plan& P, const void* d_coeffs, int64_t ld, int64_t i0, int64_t nb, cudaStream_t s);

@@ -827,7 +827,8 @@ cudaError_t launch_polar_t(const Plan& P, const void* d_images, int64_t n_img, i
 #define FBSPCA_POLAR_EXTERN(T, W, MC) \
   extern template cudaError_t launch_polar_t<T, W, MC>(const Plan&, const void*, int64_t, int64_t, cudaStream_t);
 #define FBSPCA_POLAR_LIST(X, P1, P2, P3, P4, P5, P6) \
-  P1(X(float, 6, 256)) P4(X(float, 5, 256)) P2(X(float, 6, 512)) P2(X(float, 6, 128)) P3(X(float, 6, 0)) P4(X(float, 7, 0)) P5(X(double, 13, 0)) P5(X(double, 13, 64)) P6(X(float, 6, 600)) P6(X(float, 6, 720))
+  P1(X(float, 6, 256)) P4(X(float, 5, 256)) P2(X(float, 6, 512)) P2(X(float, 6, 128)) P3(X(float, 6, 0)) P3(X(float, 5, 512)) P4(X(float, 7, 0)) \
+  P4(X(float, 5, 128)) P5(X(double, 13, 0)) P5(X(double, 13, 64)) P5(X(float, 5, 600)) P6(X(float, 6, 600)) P6(X(float, 6, 720)) P1(X(float, 5, 720))
 #define FBSPCA_ON(x) x
 #define FBSPCA_OFF(x)
 #if FBSPCA_POLAR_HERE(1)
@@ -869,23 +870,20 @@ int polar_fixed_smem(int M, int n_theta, int L, int csz, int nwarps, int nk, boo
 }
 
 cudaError_t launch_polar(const Plan& P, const void* d_images, int64_t n_img, int64_t stride, cudaStream_t s) {
-  const bool pow2 = P.n_theta == 2 * P.M && (P.M == 64 || P.M == 128 || P.M == 256 || P.M == 512 || P.M == 600 ||
-                                              P.M == 720);      // compile-time FFT kernels
   if (P.dt == FBSPCA_F64) {
     if (P.w != 13) return cudaErrorInvalidValue;
-    if (pow2 && P.M == 64) return launch_polar_t<double, 13, 64>(P, d_images, n_img, stride, s);
+    if (P.n_theta == 2 * P.M && P.M == 64) return launch_polar_t<double, 13, 64>(P, d_images, n_img, stride, s);
     return launch_polar_t<double, 13, 0>(P, d_images, n_img, stride, s);
   }
-  if (P.w == 5 && pow2 && P.M == 256) return launch_polar_t<float, 5, 256>(P, d_images, n_img, stride, s);   // eps >= 1e-4
-  if (P.w == 6 && pow2) {
-    switch (P.M) {
-      case 128: return launch_polar_t<float, 6, 128>(P, d_images, n_img, stride, s);
-      case 256: return launch_polar_t<float, 6, 256>(P, d_images, n_img, stride, s);
-      case 512: return launch_polar_t<float, 6, 512>(P, d_images, n_img, stride, s);
-      case 600: return launch_polar_t<float, 6, 600>(P, d_images, n_img, stride, s);
-      case 720: return launch_polar_t<float, 6, 720>(P, d_images, n_img, stride, s);
+  if (polar_f32_ct_kernel(P.M, P.n_theta)) {       // compile-time FFT kernels: w = 5 (eps >= 1e-4) or 6
+#define FBSPCA_CT_CASE(MC) \
+    case MC: return P.w == 5 ? launch_polar_t<float, 5, MC>(P, d_images, n_img, stride, s) \
+                             : launch_polar_t<float, 6, MC>(P, d_images, n_img, stride, s);
+    if (P.w == 5 || P.w == 6) switch (P.M) {
+      FBSPCA_CT_CASE(128) FBSPCA_CT_CASE(256) FBSPCA_CT_CASE(512) FBSPCA_CT_CASE(600) FBSPCA_CT_CASE(720)
       default: break;
     }
+#undef FBSPCA_CT_CASE
   }
   switch (P.w) {
     case 6: return launch_polar_t<float, 6, 0>(P, d_images, n_img, stride, s);

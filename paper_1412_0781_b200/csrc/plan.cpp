@@ -273,10 +273,10 @@ fbspca_status build_host_plan(Plan& P) {
   while (!smooth5(M) || M % 2) ++M;
   P.M = M;
   int w = int(std::ceil(-std::log10(P.eps) - 1e-9)) + 1;         // error ~ 10^{-(w-1)} at sigma = 2
-  // fp32: eps >= 1e-6 (the fp32 floor) -> w <= 7; eps >= 1e-4 -> w = 5 where a W = 5 kernel is compiled (M = 256 with
-  // n_theta = 2 M: the L = 128, c = 1/2 shape), else 6
+  // fp32: eps >= 1e-6 (the fp32 floor) -> w <= 7; eps >= 1e-4 -> w = 5 on the compile-time-FFT kernels (which have
+  // W = 5 instances), else 6
   if (P.dt == FBSPCA_F32) {
-    const int wmin = (M == 256 && P.n_theta == 2 * M && !getenv("FBSPCA_NO_W5")) ? 5 : 6;
+    const int wmin = (polar_f32_ct_kernel(M, P.n_theta) && !getenv("FBSPCA_NO_W5")) ? 5 : 6;
     w = std::max(wmin, std::min(w, 7));
   }
   else { w = std::max(w, 13); if (w > 13) w = 13; }
@@ -349,7 +349,9 @@ fbspca_status build_host_plan(Plan& P) {
   pp.S = S;
   // pow2 plans (n_theta = 2 M, M in {64..512}) run the ring FFTs as pairs of half-length FFTs in the per-warp
   // FFT scratch (kernels_polar.cu K3): the staging [k][ring] for 32 rings is all the region holds then
-  const bool pow2_kernel = M == 64 || M == 128 || M == 256 || M == 512 || M == 600 || M == 720;   // compile-time FFT kernels (launch_polar)
+  // fp32 compile-time FFT kernels (launch_polar's dispatch).  Only they read double entries and ring strides: an fp32
+  // plan with M = 64, or with one of these M but n_theta != 2 M (c < 1/2), runs the runtime-radix kernel on singles.
+  const bool pow2_kernel = polar_f32_ct_kernel(M, P.n_theta);
   const bool ring_pairs = P.n_theta == 2 * M && !getenv("FBSPCA_NO_RT_PAIRS");
   pp.ring_pairs = ring_pairs ? 1 : 0;
   if (ring_pairs) {

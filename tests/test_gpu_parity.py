@@ -109,10 +109,12 @@ def test_expand_rotation_reflection_on_gpu():
         assert np.max(np.abs(A[k][:, 2] - np.conj(A[k][:, 0]))) <= 1e-4 * scale
 
 
+@pytest.mark.parametrize("eps", [1e-5, 1e-4])
 @pytest.mark.parametrize("name,n", [("C4", 2), ("C5", 1), ("T3", 1), ("RB", 2)])
-def test_expand_parity_large_L(name, n):
+def test_expand_parity_large_L(name, n, eps):
     cfg, imgs = blob_case(name, 0, n)
-    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=64)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], eps=eps, device=0, max_batch=64)
+    assert plan.w == (5 if eps >= 1e-4 and name != "RB" else 6)      # RB: runtime-radix kernel, no w = 5 instance
     got = gpu_expand(plan, imgs)
     basis = O.build_basis(cfg["c"], cfg["R"])
     ref = O.to_flat(O.expand(imgs.double().cpu().numpy(), basis))

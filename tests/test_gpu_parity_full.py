@@ -106,14 +106,16 @@ def check_inputs_match_cpu_generator(cfg, imgs_gpu, sig, idx):
 
 
 # ------------------------------------------------------------------ C2 full size vs the cached oracle
-def test_c2_full_size_spectral_vs_cached_oracle():
+@pytest.mark.parametrize("eps", C3_EPS)
+def test_c2_full_size_spectral_vs_cached_oracle(eps):
     cfg = synth.config("C2")
     cache = load_cache("C2")
     n = cfg["n"]
     assert cache["n"] == n
     imgs = synth.blob_images(cfg, 0, n, device=DEV, sigma_n=cache["sigma_n"])
     check_inputs_match_cpu_generator(cfg, imgs, cache["sigma_n"], [0, 511, 512, 4097, n - 1])
-    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=BENCH_BATCH)
+    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], eps=eps, device=0, max_batch=BENCH_BATCH)
+    assert plan.w == (5 if eps >= 1e-4 else 6)
     coeffs = F.fbspca_expand(plan, imgs)
     blocks, mean = F.fbspca_covariance(plan, coeffs)
     evals, evecs = F.fbspca_eig(plan, blocks)
@@ -185,20 +187,23 @@ def test_large_L_512_image_subset(name):
     cfg = synth.config(name)
     n = 512
     imgs = synth.blob_images(cfg, 0, n, device=DEV)
-    plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], device=0, max_batch=n)
-    coeffs = F.fbspca_expand(plan, imgs)
-    blocks, mean = F.fbspca_covariance(plan, coeffs)
-    evals, evecs = F.fbspca_eig(plan, blocks)
-    torch.cuda.synchronize()
     basis = O.build_basis(cfg["c"], cfg["R"])
     A = O.expand(imgs.double().cpu().numpy(), basis)
-    got = coeffs.cpu().numpy().astype(np.complex128)
-    rel = rel_l2_per_image(got, O.to_flat(A), basis)
-    print(f"{name} 512 images: max rel l2 {rel.max():.3e}")
-    assert rel.max() <= TOL32, f"{name}: max per-image rel l2 {rel.max():.3e}"
     m_o, C_o = O.block_covariance(A)
     lam_o, U_o = O.block_eig(C_o)
-    spectral_checks(plan, blocks, mean, evals, evecs, m_o, C_o, lam_o, U_o)
+    for eps in C3_EPS:                                  # w = 6 (library default) and w = 5 (bench.py's eps)
+        plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], eps=eps, device=0, max_batch=n)
+        assert plan.w == (5 if eps >= 1e-4 else 6)
+        coeffs = F.fbspca_expand(plan, imgs)
+        blocks, mean = F.fbspca_covariance(plan, coeffs)
+        evals, evecs = F.fbspca_eig(plan, blocks)
+        torch.cuda.synchronize()
+        got = coeffs.cpu().numpy().astype(np.complex128)
+        rel = rel_l2_per_image(got, O.to_flat(A), basis)
+        print(f"{name} 512 images, w = {plan.w}: max rel l2 {rel.max():.3e}")
+        assert rel.max() <= TOL32, f"{name}: max per-image rel l2 {rel.max():.3e}"
+        spectral_checks(plan, blocks, mean, evals, evecs, m_o, C_o, lam_o, U_o)
+        del plan, coeffs
 
 
 # ------------------------------------------------------------------ K7 on every component, modes 0/1/2
@@ -268,13 +273,13 @@ def test_eigenimages_parity():
 @pytest.mark.parametrize("name,n,eps", [("C2", 40, 1e-6), ("C3", 8, 1e-6), ("C2", 40, 1e-5), ("C3", 8, 1e-4),
                                           ("C3", 150, 1e-3), ("C2", 40, 1e-4)])
 def test_eps_contract_fp32(name, n, eps):
-    """fbspca_plan's eps: w = ceil(log10(1/eps)) + 1 taps (fp32: clamped to [6, 7], and [5, 7] on the M = 256 kernel
-    -- C3's shape -- which has a w = 5 instance for eps >= 1e-4); eps = 1e-6 selects the w = 7 runtime-radix polar
+    """fbspca_plan's eps: w = ceil(log10(1/eps)) + 1 taps (fp32: clamped to [5, 7] on the compile-time-FFT kernels,
+    which have w = 5 instances for eps >= 1e-4, and to [6, 7] on the runtime-radix kernel); eps = 1e-6 selects the w = 7 runtime-radix polar
     kernel.  Contract (include/fbspca.h): per-image coefficient rel l2 <= max(4 eps, 4e-6)."""
     cfg = synth.config(name)
     imgs = synth.blob_images(cfg, 0, n, device=DEV)
     plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], eps=eps, device=0, max_batch=64)
-    assert plan.w == (7 if eps <= 1e-6 else 5 if (eps >= 1e-4 and name == "C3") else 6)
+    assert plan.w == (7 if eps <= 1e-6 else 5 if eps >= 1e-4 else 6)
     got = F.fbspca_expand(plan, imgs).cpu().numpy().astype(np.complex128)
     basis = O.build_basis(cfg["c"], cfg["R"])
     ref = O.to_flat(O.expand(imgs.double().cpu().numpy(), basis))
@@ -285,17 +290,37 @@ def test_eps_contract_fp32(name, n, eps):
 
 @pytest.mark.parametrize("L,R", [(33, 16), (40, 20), (27, 13)])
 def test_expand_fp64_runtime_radix(L, R):
-    """fp64 plans with M != 64 run polar_kernel<double, 13, 0> (runtime mixed radices: M = 72, 80, 54)."""
+    _runtime_radix(L, 0.5, R, F.F64, 1e-9)
+
+
+@pytest.mark.parametrize("L,c,R", [(32, 0.5, 16), (64, 0.3, 32), (128, 0.25, 64), (33, 0.5, 16)])
+def test_expand_fp32_runtime_kernel_shapes(L, c, R):
+    """fp32 plans the compile-time-FFT kernels do not serve although M is one of their sizes or a power of two:
+    M = 64, and n_theta != 2 M (c < 1/2).  They run polar_kernel<float, 6, 0> on single entries and full rings (the
+    plan must not emit double entries or ring strides for them: internal.h polar_f32_ct_kernel)."""
+    for eps in (1e-5, 1e-4):
+        _runtime_radix(L, c, R, F.F32, TOL32, eps)
+
+
+def _runtime_radix(L, c, R, dt, tol, eps=0.0):
+    """fp64 plans with M != 64 run polar_kernel<double, 13, 0> (runtime mixed radices: M = 72, 80, 54); the fp32
+    shapes above run polar_kernel<float, 6, 0>.  White-noise images, every coefficient against the oracle."""
     rng = np.random.default_rng(L)
     imgs = rng.standard_normal((6, L, L))
-    plan = F.fbspca_plan(L, 0.5, R, dtype=F.F64, device=0, max_batch=4)
-    assert plan.M != 64
-    got = F.fbspca_expand(plan, torch.from_numpy(imgs).to(DEV)).cpu().numpy()
-    basis = O.build_basis(0.5, R)
+    plan = F.fbspca_plan(L, c, R, eps=eps, dtype=dt, device=0, max_batch=4)
+    if dt == F.F64:
+        assert plan.M != 64
+        x = torch.from_numpy(imgs).to(DEV)
+    else:
+        assert plan.w == 6                       # no w = 5 instance of the runtime-radix kernel
+        imgs = imgs.astype(np.float32).astype(np.float64)
+        x = torch.from_numpy(imgs).to(DEV, torch.float32)
+    got = F.fbspca_expand(plan, x).cpu().numpy().astype(np.complex128)
+    basis = O.build_basis(c, R)
     ref = O.to_flat(O.expand(imgs, basis))
     rel = rel_l2_per_image(got, ref, basis)
-    print(f"fp64 L={L} M={plan.M}: max rel l2 {rel.max():.3e}")
-    assert rel.max() <= 1e-9
+    print(f"{'fp64' if dt == F.F64 else 'fp32'} L={L} c={c} M={plan.M} n_theta={plan.n_theta}: max rel l2 {rel.max():.3e}")
+    assert rel.max() <= tol
 
 
 # ------------------------------------------------------------------ K5 on tcgen05 for 128 < p_k <= 256

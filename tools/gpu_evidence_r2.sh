@@ -4,6 +4,7 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 timeout 900 python bench.py > gpurun_out/ev_bench_C3.json 2> gpurun_out/ev_bench_C3.err; echo "C3 rc=$?"
+timeout 900 python bench.py --eps 1e-5 --no-cpu-baseline --no-e2e > gpurun_out/ev_bench_C3_eps1e-5.json 2> gpurun_out/ev_bench_C3_eps1e-5.err; echo "C3 eps 1e-5 (w = 6) rc=$?"
 for cfg in T3 C5 RB C2; do
   timeout 900 python bench.py --config $cfg --no-cpu-baseline --no-e2e > gpurun_out/ev_bench_$cfg.json 2> gpurun_out/ev_bench_$cfg.err
   echo "$cfg rc=$?"
