@@ -69,8 +69,7 @@ typedef enum { FBSPCA_F32 = 0, FBSPCA_F64 = 1 } fbspca_dtype;
  *            2L and n_theta must factor into 2, 3, 5, 7, 11, 13 and n_theta must be even, else FBSPCA_ERR_CONFIG.
  *   eps      NUFFT accuracy target, [1e-14, 1e-3]; <= 0 picks the default (1e-5 for F32, 1e-12 for F64).
  *            F32 rejects eps < 1e-6.  The window gets w = ceil(log10(1/eps)) + 1 taps per axis at oversampling ~2
- *            (F32: clamped to [5, 7] where n_theta = 2M and M is 128, 256, 512, 600 or 720 -- the shapes with
- *            compile-time-FFT kernels -- and to [6, 7] elsewhere; F64: 13), which holds the per-image coefficient
+ *            (F32: clamped to [5, 7]; F64: 13), which holds the per-image coefficient
  *            relative l2 error against the exact Fourier sum (reading Q12) to <= max(4 eps, 4e-6) for F32
  *            (measured at L = 128: 6.0e-5 at eps = 1e-4 / w = 5, 5.8e-6 at the default 1e-5 / w = 6, 1.3e-6 at
  *            1e-6 / w = 7; tests/test_gpu_parity_full.py) and <= 1e-9 for F64.

@@ -199,7 +199,7 @@ cudaError_t launch_project(const Plan& P, const void* d_coeffs, int64_t n, const
                            int64_t n_total, void* d_out, cudaStream_t s);
 // fp32 plans served by a compile-time-FFT polar kernel (launch_polar's dispatch; the plan emits double entries and
 // ring strides only for these -- the runtime-radix kernel gathers single entries on full rings).  Window widths
-// w = 5 (eps >= 1e-4) and w = 6 are compiled for every such M.
+// w = 5 (eps >= 1e-4) and w = 6 are compiled for every such M and for the runtime-radix kernel; w = 7 only for the latter.
 inline bool polar_f32_ct_kernel(int M, int n_theta) {
   return n_theta == 2 * M && (M == 128 || M == 256 || M == 512 || M == 600 || M == 720);
 }

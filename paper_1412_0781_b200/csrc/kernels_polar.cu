@@ -827,7 +827,7 @@ cudaError_t launch_polar_t(const Plan& P, const void* d_images, int64_t n_img, i
 #define FBSPCA_POLAR_EXTERN(T, W, MC) \
   extern template cudaError_t launch_polar_t<T, W, MC>(const Plan&, const void*, int64_t, int64_t, cudaStream_t);
 #define FBSPCA_POLAR_LIST(X, P1, P2, P3, P4, P5, P6) \
-  P1(X(float, 6, 256)) P4(X(float, 5, 256)) P2(X(float, 6, 512)) P2(X(float, 6, 128)) P3(X(float, 6, 0)) P3(X(float, 5, 512)) P4(X(float, 7, 0)) \
+  P1(X(float, 6, 256)) P4(X(float, 5, 256)) P2(X(float, 6, 512)) P2(X(float, 6, 128)) P3(X(float, 6, 0)) P3(X(float, 5, 512)) P6(X(float, 5, 0)) P4(X(float, 7, 0)) \
   P4(X(float, 5, 128)) P5(X(double, 13, 0)) P5(X(double, 13, 64)) P5(X(float, 5, 600)) P6(X(float, 6, 600)) P6(X(float, 6, 720)) P1(X(float, 5, 720))
 #define FBSPCA_ON(x) x
 #define FBSPCA_OFF(x)
@@ -886,6 +886,7 @@ cudaError_t launch_polar(const Plan& P, const void* d_images, int64_t n_img, int
 #undef FBSPCA_CT_CASE
   }
   switch (P.w) {
+    case 5: return launch_polar_t<float, 5, 0>(P, d_images, n_img, stride, s);   // eps >= 1e-4
     case 6: return launch_polar_t<float, 6, 0>(P, d_images, n_img, stride, s);
     case 7: return launch_polar_t<float, 7, 0>(P, d_images, n_img, stride, s);   // eps = 1e-6 (the fp32 floor)
     default: return cudaErrorInvalidValue;

@@ -273,12 +273,9 @@ fbspca_status build_host_plan(Plan& P) {
   while (!smooth5(M) || M % 2) ++M;
   P.M = M;
   int w = int(std::ceil(-std::log10(P.eps) - 1e-9)) + 1;         // error ~ 10^{-(w-1)} at sigma = 2
-  // fp32: eps >= 1e-6 (the fp32 floor) -> w <= 7; eps >= 1e-4 -> w = 5 on the compile-time-FFT kernels (which have
-  // W = 5 instances), else 6
-  if (P.dt == FBSPCA_F32) {
-    const int wmin = (polar_f32_ct_kernel(M, P.n_theta) && !getenv("FBSPCA_NO_W5")) ? 5 : 6;
-    w = std::max(wmin, std::min(w, 7));
-  }
+  // fp32: eps >= 1e-6 (the fp32 floor) -> w <= 7; eps >= 1e-4 -> w = 5 (every fp32 polar kernel has W = 5, 6 instances;
+  // W = 7 runs the runtime-radix kernel)
+  if (P.dt == FBSPCA_F32) w = std::max(getenv("FBSPCA_NO_W5") ? 6 : 5, std::min(w, 7));
   else { w = std::max(w, 13); if (w > 13) w = 13; }
   P.w = w;
   P.beta = 2.30 * w;

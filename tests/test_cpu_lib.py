@@ -70,16 +70,16 @@ def test_plan_window_and_phases():
     assert 1 <= pl.n_phase <= 4 and pl.smem_bytes <= 227 * 1024
     pl64 = F.fbspca_plan(32, 0.5, 16, dtype=F.F64, device=-1)
     assert pl64.w == 13
-    # eps >= 1e-4: w = 5 on the compile-time-FFT kernels' shapes (n_theta = 2 M, M in {128, 256, 512, 600, 720}),
-    # 6 on the runtime-radix kernel (M = 64; c < 1/2; other M); eps = 1e-6: w = 7
+    # eps >= 1e-4: w = 5 (compile-time-FFT and runtime-radix kernels alike); eps = 1e-6: w = 7
     pl5 = F.fbspca_plan(128, 0.5, 64, eps=1e-4, device=-1)
     assert pl5.w == 5 and pl5.M == 256 and abs(pl5.beta - float(np.float32(2.3 * 5))) < 1e-12
     assert pl5.n_phase == pl.n_phase and pl5.smem_bytes <= 227 * 1024
     assert F.fbspca_plan(64, 0.5, 32, eps=1e-4, device=-1).w == 5
     assert F.fbspca_plan(300, 0.5, 150, eps=1e-4, device=-1).w == 5
-    assert F.fbspca_plan(32, 0.5, 16, eps=1e-4, device=-1).w == 6
-    assert F.fbspca_plan(128, 0.25, 64, eps=1e-4, device=-1).w == 6
-    assert F.fbspca_plan(240, 0.196, 98, eps=1e-4, device=-1).w == 6
+    assert F.fbspca_plan(32, 0.5, 16, eps=1e-4, device=-1).w == 5
+    assert F.fbspca_plan(128, 0.25, 64, eps=1e-4, device=-1).w == 5
+    assert F.fbspca_plan(240, 0.196, 98, eps=1e-4, device=-1).w == 5
+    assert F.fbspca_plan(240, 0.196, 98, device=-1).w == 6
     assert F.fbspca_plan(128, 0.5, 64, eps=1e-6, device=-1).w == 7
 
 

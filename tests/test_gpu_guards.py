@@ -50,7 +50,8 @@ def check(buf, what):
 CASES = [("C2", 64, 0.5, 32.0, F.F32, 0.0, 40), ("C2e6", 64, 0.5, 32.0, F.F32, 1e-6, 24),
          ("fp64-64", 32, 0.5, 16.0, F.F64, 0.0, 20), ("fp64-72", 33, 0.5, 16.0, F.F64, 0.0, 12),
          ("C3", 128, 0.5, 64.0, F.F32, 0.0, 300), ("C3w5", 128, 0.5, 64.0, F.F32, 1e-4, 300),
-         ("C2w5", 64, 0.5, 32.0, F.F32, 1e-4, 40), ("f32-64", 32, 0.5, 16.0, F.F32, 0.0, 20)]
+         ("C2w5", 64, 0.5, 32.0, F.F32, 1e-4, 40), ("f32-64", 32, 0.5, 16.0, F.F32, 0.0, 20),
+         ("f32-64w5", 32, 0.5, 16.0, F.F32, 1e-4, 20)]
 
 
 @pytest.mark.parametrize("name,L,c,R,dt,eps,n", CASES)

@@ -114,7 +114,7 @@ def test_expand_rotation_reflection_on_gpu():
 def test_expand_parity_large_L(name, n, eps):
     cfg, imgs = blob_case(name, 0, n)
     plan = F.fbspca_plan(cfg["L"], cfg["c"], cfg["R"], eps=eps, device=0, max_batch=64)
-    assert plan.w == (5 if eps >= 1e-4 and name != "RB" else 6)      # RB: runtime-radix kernel, no w = 5 instance
+    assert plan.w == (5 if eps >= 1e-4 else 6)
     got = gpu_expand(plan, imgs)
     basis = O.build_basis(cfg["c"], cfg["R"])
     ref = O.to_flat(O.expand(imgs.double().cpu().numpy(), basis))

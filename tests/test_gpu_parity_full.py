@@ -273,8 +273,8 @@ def test_eigenimages_parity():
 @pytest.mark.parametrize("name,n,eps", [("C2", 40, 1e-6), ("C3", 8, 1e-6), ("C2", 40, 1e-5), ("C3", 8, 1e-4),
                                           ("C3", 150, 1e-3), ("C2", 40, 1e-4)])
 def test_eps_contract_fp32(name, n, eps):
-    """fbspca_plan's eps: w = ceil(log10(1/eps)) + 1 taps (fp32: clamped to [5, 7] on the compile-time-FFT kernels,
-    which have w = 5 instances for eps >= 1e-4, and to [6, 7] on the runtime-radix kernel); eps = 1e-6 selects the w = 7 runtime-radix polar
+    """fbspca_plan's eps: w = ceil(log10(1/eps)) + 1 taps (fp32: clamped to [5, 7]; eps >= 1e-4 selects the w = 5
+    instances); eps = 1e-6 selects the w = 7 runtime-radix polar
     kernel.  Contract (include/fbspca.h): per-image coefficient rel l2 <= max(4 eps, 4e-6)."""
     cfg = synth.config(name)
     imgs = synth.blob_images(cfg, 0, n, device=DEV)
@@ -296,7 +296,7 @@ def test_expand_fp64_runtime_radix(L, R):
 @pytest.mark.parametrize("L,c,R", [(32, 0.5, 16), (64, 0.3, 32), (128, 0.25, 64), (33, 0.5, 16)])
 def test_expand_fp32_runtime_kernel_shapes(L, c, R):
     """fp32 plans the compile-time-FFT kernels do not serve although M is one of their sizes or a power of two:
-    M = 64, and n_theta != 2 M (c < 1/2).  They run polar_kernel<float, 6, 0> on single entries and full rings (the
+    M = 64, and n_theta != 2 M (c < 1/2).  They run polar_kernel<float, 5 or 6, 0> on single entries and full rings (the
     plan must not emit double entries or ring strides for them: internal.h polar_f32_ct_kernel)."""
     for eps in (1e-5, 1e-4):
         _runtime_radix(L, c, R, F.F32, TOL32, eps)
@@ -312,7 +312,7 @@ def _runtime_radix(L, c, R, dt, tol, eps=0.0):
         assert plan.M != 64
         x = torch.from_numpy(imgs).to(DEV)
     else:
-        assert plan.w == 6                       # no w = 5 instance of the runtime-radix kernel
+        assert plan.w == (5 if eps >= 1e-4 else 6)
         imgs = imgs.astype(np.float32).astype(np.float64)
         x = torch.from_numpy(imgs).to(DEV, torch.float32)
     got = F.fbspca_expand(plan, x).cpu().numpy().astype(np.complex128)
