@@ -8,7 +8,7 @@ VARS="A $*"
 for r in 1 2; do
   for v in $VARS; do
     if [ $v = A ]; then unset FBSPCA_LIB; else export FBSPCA_LIB=$PWD/paper_1412_0781_b200/lib_$v/libfbspca.so; fi
-    timeout 600 python bench.py --config $CFG $EXTRA --steps 8 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > gpurun_out/ab_$v$r.json 2> gpurun_out/ab_$v$r.err
+    timeout 600 python bench.py --config $CFG $EXTRA --steps 8 --warmup 3 --no-e2e --no-cpu-baseline --no-graph --no-default-eps > gpurun_out/ab_$v$r.json 2> gpurun_out/ab_$v$r.err
     python - $v$r <<'PY'
 import json, sys
 try:

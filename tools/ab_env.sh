@@ -7,7 +7,7 @@ for r in 1 2; do
   for v in base "$@"; do
     if [ "$v" = base ]; then envs=""; else envs=$(echo "$v" | tr ',' ' '); fi
     tag=$(echo "$v" | tr '=,' '__')
-    env $envs timeout 600 python bench.py --config $CFG --steps 8 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > gpurun_out/abe_$tag$r.json 2> gpurun_out/abe_$tag$r.err
+    env $envs timeout 600 python bench.py --config $CFG --steps 8 --warmup 3 --no-e2e --no-cpu-baseline --no-graph --no-default-eps > gpurun_out/abe_$tag$r.json 2> gpurun_out/abe_$tag$r.err
     python - "$tag$r" <<'PY'
 import json, sys
 try:

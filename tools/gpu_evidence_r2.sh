@@ -12,7 +12,7 @@ done
 timeout 900 python bench.py --config C4 --n 100000 --no-cpu-baseline --no-e2e > gpurun_out/ev_bench_C4.json 2> gpurun_out/ev_bench_C4.err; echo "C4 rc=$?"
 timeout 600 python bench.py --nccl --no-cpu-baseline --no-e2e > gpurun_out/ev_bench_nccl.json 2> gpurun_out/ev_bench_nccl.err; echo "nccl rc=$?"
 python tools/time_extras.py > gpurun_out/ev_extras.json 2>&1; echo "extras rc=$?"
-CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-graph"
+CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-graph --no-default-eps"
 $CMD > gpurun_out/ev_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"polar|radial|cov_|finalize" -c 400 --csv \
     --log-file gpurun_out/ev_launches.csv $CMD > gpurun_out/ev_ncu_launches.log 2>&1

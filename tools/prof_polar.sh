@@ -5,7 +5,7 @@ cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 TAG=${1:-polar}
 shift
-CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --n 16384 --batch 16384 $*"
+CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-default-eps --n 16384 --batch 16384 $*"
 timeout 300 $CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"polar_kernel" -s 1 -c 1 \
     -o gpurun_out/${TAG} $CMD > gpurun_out/${TAG}_ncu.log 2>&1

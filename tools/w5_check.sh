@@ -4,7 +4,7 @@ cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 timeout 900 python tools/w5_probe.py 512 > gpurun_out/w5_probe.log 2>&1; echo "probe rc=$?"; cat gpurun_out/w5_probe.log | tail -3
 for r in 1 2; do for e in 1e-5 1e-4; do
-  timeout 600 python bench.py --eps $e --steps 8 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > gpurun_out/w5_bench_${e}_$r.json 2> gpurun_out/w5_bench_${e}_$r.err
+  timeout 600 python bench.py --eps $e --steps 8 --warmup 3 --no-e2e --no-cpu-baseline --no-graph --no-default-eps > gpurun_out/w5_bench_${e}_$r.json 2> gpurun_out/w5_bench_${e}_$r.err
   python - $e $r <<'PY'
 import json, sys
 try:
