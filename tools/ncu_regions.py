@@ -8,7 +8,7 @@ import sys
 def _find_regions():
     src = open("/root/repo/paper_1412_0781_b200/csrc/kernels_polar.cu").read().splitlines()
     marks = [("K1a: row FFTs", "image/row FFT"), ("per phase: K1b column FFTs", "col fill"), ("PROF_MARK(1);", "col FFT"),
-             ("if constexpr (sizeof(T) == 4 && W == 6 && MC > 0)", "gather doubles"),
+             ("if constexpr (sizeof(T) == 4 && (W == 5 || W == 6) && MC > 0)", "gather doubles"),
              ("const int nb = pp.phase_node_begin[ph]", "gather singles"), ("const bool want_prefetch", "ring FFT"),
              ("const int64_t kstride = pp.ghat_kstride", "write-out"), ("PROF_STORE();", "tail")]
     out = [(0, "setup")]
